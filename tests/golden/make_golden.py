@@ -1,0 +1,141 @@
+"""Generate golden fixtures by running the REAL reference (build container only).
+
+    python tests/golden/make_golden.py
+
+Imports /root/reference/pkg/src/samp (staged with the restated tokenizer, see
+refimport.py) and records, for a few deterministic synthetic models:
+  * the archive recipe (build_archive kwargs) and its SHA-256 fingerprint, so
+    tests can regenerate identical weights without storing them;
+  * the reference calibration table (Engine.calibrate);
+  * inputs, and for each precision plan the reference Engine.run hidden
+    states, taps (capture_taps=True) and head outputs.
+Outputs go to tests/golden/*.npz + *.json.  Nothing here runs on the GPU box.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+from refimport import load_reference  # noqa: E402
+
+samp = load_reference()
+from samp.encoder import Engine, PrecisionPlan  # noqa: E402
+from samp.synthetic import build_archive, calibrated_archive, tiny_vocab  # noqa: E402
+from samp.tasks import classify, tag  # noqa: E402
+from samp.tokenization import EncodedInput  # noqa: E402
+
+
+def random_inputs(vocab_size, specs, seed):
+    """specs: list of (padded_len, att_len); ids past att_len are [PAD]=2."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for total, att in specs:
+        ids = rng.integers(4, vocab_size, size=att).tolist() + [2] * (total - att)
+        segs = [0] * total
+        out.append(EncodedInput(ids, segs, att))
+    return out
+
+
+def dump_case(name, recipe, task, plans, inputs, calib_inputs=None, fp16_modes=(False,), taps_plan=None):
+    vocab = recipe.pop("vocab_extra", None)
+    kwargs = dict(recipe)
+    if vocab is not None:
+        kwargs["vocab"] = tiny_vocab(max_seq_len=kwargs["max_position"], extra_tokens=vocab)
+    if calib_inputs is None:
+        arch = calibrated_archive(task=task, **kwargs)
+    else:
+        arch = build_archive(task=task, **kwargs)
+        arch.calibration = Engine(arch).calibrate(calib_inputs)
+    arrays = {}
+    meta = {
+        "name": name,
+        "recipe": {k: v for k, v in recipe.items()},
+        "vocab_extra": len(vocab) if vocab is not None else 0,
+        "task": task,
+        "fingerprint": arch.fingerprint,
+        "amax": {s: e.amax for s, e in arch.calibration.entries.items()},
+        "inputs": [{"ids": e.token_ids, "segs": e.segment_ids, "att": e.attention_length} for e in inputs],
+        "runs": [],
+    }
+    for fp16 in fp16_modes:
+        eng = Engine(arch, fp16_storage=fp16)
+        for mode, k in plans:
+            plan = PrecisionPlan.prefix(mode, arch.manifest.num_layers, k)
+            for j, enc in enumerate(inputs):
+                want_taps = taps_plan == (mode, k) and not fp16 and j == 0
+                out = eng.run(enc, plan, capture_taps=want_taps)
+                key = f"{mode}.{k}.{int(fp16)}.{j}"
+                arrays[f"hidden/{key}"] = out.hidden_states
+                run = {"mode": mode, "k": k, "fp16": fp16, "input": j, "key": key}
+                if task == "sequence_labeling":
+                    res = tag(arch, out, enc.attention_length)
+                else:
+                    res = classify(arch, out)
+                run["labels"] = res.label_ids
+                arrays[f"logits/{key}"] = np.asarray(res.logits, dtype=np.float32)
+                arrays[f"probs/{key}"] = np.asarray(res.scores, dtype=np.float32)
+                if want_taps:
+                    for site, val in out.taps.items():
+                        arrays[f"taps/{key}/{site}"] = val
+                    run["taps"] = sorted(out.taps)
+                meta["runs"].append(run)
+    # big arrays are pinned by SHA-256 of their float32 bytes (+ a head slice
+    # for diagnostics) to keep the committed fixtures small
+    small, digests = {}, {}
+    for key, val in arrays.items():
+        val = np.ascontiguousarray(val)
+        if val.nbytes <= 64 * 1024:
+            small[key] = val
+        else:
+            digests[key] = {"sha256": hashlib.sha256(val.tobytes()).hexdigest(),
+                            "shape": list(val.shape), "dtype": str(val.dtype)}
+            small[f"head/{key}"] = val.reshape(-1)[:512]
+    meta["digests"] = digests
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **small)
+    with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print(name, "runs", len(meta["runs"]), "arrays", len(arrays))
+
+
+def main():
+    # 1. the reference's own tiny_cls model (fingerprint 7ede3e3d...; reference tests/conftest.py:8-10)
+    from samp.synthetic import SAMPLE_TEXTS
+    arch_tmp = calibrated_archive(seed=0)
+    eng = Engine(arch_tmp)
+    tiny_inputs = [eng.encode_text(t) for t in SAMPLE_TEXTS[:4]]
+    plans = [("FP", 0), ("FULLY_QUANT", 1), ("FULLY_QUANT", 2), ("FFN_ONLY", 1), ("FFN_ONLY", 2)]
+    dump_case("tiny_cls", dict(seed=0, num_layers=2, hidden=8, num_heads=2, intermediate=16,
+                               max_position=16), "classification", plans, tiny_inputs,
+              fp16_modes=(False, True), taps_plan=("FULLY_QUANT", 2))
+
+    # 2. mini model at GPU-legal shapes (head_dim 64), padded and unpadded inputs
+    extra = [f"w{i}" for i in range(456)]   # vocab 500
+    recipe = dict(seed=7, num_layers=2, hidden=128, num_heads=2, intermediate=256, max_position=64,
+                  weight_scale=0.08, vocab_extra=extra)
+    calib = random_inputs(500, [(64, 64), (64, 50), (64, 33), (64, 64)], seed=11)
+    inputs = random_inputs(500, [(64, 64), (64, 40), (64, 17)], seed=12)
+    plans = [("FP", 0), ("FULLY_QUANT", 1), ("FULLY_QUANT", 2), ("FFN_ONLY", 2)]
+    dump_case("mini", recipe, "classification", plans, inputs, calib_inputs=calib,
+              taps_plan=("FULLY_QUANT", 2))
+
+    # 3. one BERT-base-shaped layer (H=768, 12 heads, I=3072) at S=128: pins the
+    #    768-wide LN tree and the 128-key softmax tree at the real sizes
+    extra = [f"w{i}" for i in range(1000 - 44)]
+    recipe = dict(seed=3, num_layers=1, hidden=768, num_heads=12, intermediate=3072, max_position=128,
+                  weight_scale=0.02, vocab_extra=extra)
+    calib = random_inputs(1000, [(128, 128), (128, 100)], seed=21)
+    inputs = random_inputs(1000, [(128, 128), (128, 77)], seed=22)
+    plans = [("FULLY_QUANT", 1), ("FFN_ONLY", 1)]
+    dump_case("base1", recipe, "sequence_labeling", plans, inputs, calib_inputs=calib,
+              taps_plan=("FULLY_QUANT", 1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,124 @@
+/*
+ * samp_b200 — C ABI of the B200-native SAMP mixed-precision encoder.
+ *
+ * The reference has no FFI: its hot path is the Python API
+ *   Engine(archive, fp16_storage)            reference pkg/src/samp/encoder.py:424-431
+ *   Engine.run(enc, plan, capture_taps)      reference pkg/src/samp/encoder.py:472-530
+ *   Engine.quantized_layer / check_plan      reference pkg/src/samp/encoder.py:437-470
+ *   classify / tag                           reference pkg/src/samp/tasks.py:28-55
+ *   Engine.calibrate                         reference pkg/src/samp/encoder.py:446-454
+ * Every entry point below is what that API binds to in paper_2209_09130_b200
+ * (Python ctypes, _lib.py); INTEGRATION.md shows the binding a maintainer of
+ * the reference would add.  Plain pointers and sizes only; no torch types.
+ *
+ * Errors: every call returns SAMP_OK or one SAMP_E_* code that maps 1:1 onto
+ * the reference's exception classes (errors.py:4-41); the message is in
+ * samp_last_error() (thread-local).  All validation happens before any
+ * device work, as in the reference.
+ */
+#ifndef SAMP_B200_H
+#define SAMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exception classes */
+#define SAMP_OK              0
+#define SAMP_E_DIMENSION     1  /* DimensionError      */
+#define SAMP_E_CONFIGURATION 2  /* ConfigurationError  */
+#define SAMP_E_CALIBRATION   3  /* CalibrationError    */
+#define SAMP_E_INPUT         4  /* InputError          */
+#define SAMP_E_DEVICE        5  /* (new) CUDA failure / no B200 */
+#define SAMP_E_INTERNAL      6
+
+/* per-layer precision codes (reference encoder.py:50-52 + MHA-only extension) */
+#define SAMP_LAYER_FP        0  /* "FP"             */
+#define SAMP_LAYER_FFN_INT8  1  /* "FFN_ONLY_INT8"  */
+#define SAMP_LAYER_FULL_INT8 2  /* "FULL_INT8"      */
+#define SAMP_LAYER_MHA_INT8  3  /* "MHA_ONLY_INT8"  (extension) */
+
+/* heads (reference tasks.py) */
+#define SAMP_HEAD_NONE     0
+#define SAMP_HEAD_CLASSIFY 1    /* pooled [CLS] tanh pooler + classifier + softmax + argmax */
+#define SAMP_HEAD_TAG      2    /* per-token classifier + softmax + argmax */
+
+/* samp_forward io flags */
+#define SAMP_IO_HOST   0        /* ids/segs/outputs are host pointers (copies inside the call) */
+#define SAMP_IO_DEVICE 1        /* ids/segs/outputs are device pointers on the engine's GPU   */
+
+typedef struct samp_engine samp_engine;
+
+typedef struct samp_model_desc {
+  int32_t num_layers, hidden, num_heads, intermediate;
+  int32_t vocab_size, max_position, type_vocab_size, num_labels;
+  double layernorm_eps;
+  int32_t fp16_storage;     /* reference Engine(fp16_storage=...) */
+} samp_model_desc;
+
+typedef struct samp_outputs {
+  float* hidden;    /* [T][hidden] final hidden states, or NULL */
+  float* logits;    /* CLASSIFY: [nseq][num_labels]; TAG: [T][num_labels]; or NULL */
+  float* probs;     /* same shape as logits, or NULL */
+  int32_t* labels;  /* CLASSIFY: [nseq]; TAG: [T]; or NULL */
+  int32_t head;     /* SAMP_HEAD_* */
+} samp_outputs;
+
+const char* samp_last_error(void);
+int samp_device_check(int device);       /* SAMP_OK if `device` is an sm_100 GPU */
+
+/* Engine(archive) — replaces reference encoder.py:424-431 */
+int samp_engine_create(const samp_model_desc* desc, int device, samp_engine** out);
+void samp_engine_destroy(samp_engine* e);
+
+/* weight upload from the archive layout (F32, matrices (in, out) row-major,
+ * reference archive.py:95-134); INT8 copies use quantize_weight (encoder.py:191-194) */
+int samp_load_embeddings(samp_engine* e, const float* word, const float* position, const float* token_type,
+                         const float* ln_gamma, const float* ln_beta);
+/* t[16] = qw qb kw kb vw vb ow ob attn_ln_g attn_ln_b w1 b1 w2 b2 ffn_ln_g ffn_ln_b */
+int samp_load_layer(samp_engine* e, int layer, const float* const* t);
+int samp_load_heads(samp_engine* e, const float* pooler_w, const float* pooler_b,
+                    const float* head_w, const float* head_b);
+/* per-tensor INT8 weight scales the engine derived (encoder.py:191-225):
+ * out[6] = s_qw, s_kw, s_vw, s_ow, s_w1, s_w2 */
+int samp_weight_scales(samp_engine* e, int layer, double* out6);
+
+/* calibration table -> site scales (quantization.py:72-80); site names as encoder.py:60-83 */
+int samp_set_site_amax(samp_engine* e, const char* site, double amax);
+int samp_clear_calibration(samp_engine* e);
+
+/* Engine.run over a packed batch of nseq sequences.
+ *   layer_prec[num_layers]: SAMP_LAYER_* (validated like PrecisionPlan + check_plan)
+ *   seq_start[nseq+1] (host): packed row offsets; sequence s owns rows
+ *       [seq_start[s], seq_start[s+1]) (its full, possibly padded, length)
+ *   att_len[nseq] (host): non-pad prefix length (reference EncodedInput.attention_length)
+ *   ids, segs [T]: token / segment ids (host or device per io)
+ *   stream: cudaStream_t or NULL for the engine's stream */
+int samp_forward(samp_engine* e, const uint8_t* layer_prec, int32_t nseq, const int32_t* seq_start,
+                 const int32_t* att_len, const int32_t* ids, const int32_t* segs, int32_t io,
+                 const samp_outputs* out, void* stream);
+
+/* synchronise the engine's stream */
+int samp_sync(samp_engine* e);
+
+/* Debug/parity: after samp_forward with samp_set_capture(e, 1), copy the named
+ * stage buffer of `layer` (names in DESIGN.md: in_q, qkv_q, ctx_q, ffn_in_q, mid_q,
+ * out_q, out_f32, embed_f32, ...) to host; *bytes receives the size. */
+int samp_set_capture(samp_engine* e, int on);
+int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, size_t capacity, size_t* bytes);
+
+/* kernel-level parity entry points (host pointers; allocate + copy internally).
+ * B is given in the reference layout [k][n] row-major (activation @ weight). */
+int samp_debug_gemm_i8(const int8_t* a, const int8_t* b, int32_t* c, int m, int n, int k);
+int samp_debug_gemm_f16(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);
+
+/* number of kernel launches issued by the last samp_forward (for bench gpu_launches) */
+int samp_last_launch_count(samp_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAMP_B200_H */

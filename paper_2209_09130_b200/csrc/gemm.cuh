@@ -1,0 +1,458 @@
+// Warp-specialised tcgen05 GEMM for the encoder's four projections.
+//
+//   C[M, N] = A[M, K] * W[K, N]   A: activations, row-major [M][K] (K-major)
+//                                 W: weights stored transposed Wt[N][K] (K-major)
+//
+// One CTA computes a 128 x BN tile (UMMA M=128, N=BN, cta_group::1); int32 (kind::i8)
+// or f32 (kind::f16) accumulators live in TMEM.  Warp roles (192 threads):
+//   warp 0     TMA producer: 128B-swizzled A/B k-blocks (128 bytes of K) into a
+//              STAGES-deep smem ring, completion on full[] mbarriers
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs of 32 B of K
+//              per k-block); tcgen05.commit frees ring slots and finally signals tmem_full
+//   warps 2-5  epilogue: thread t owns accumulator row t (TMEM lane t) and streams its
+//              row out of TMEM with tcgen05.ld.32x32b — a whole output row per thread is
+//              what lets the fused LayerNorm epilogue reproduce numpy's pairwise tree
+//              sequentially, bit-for-bit (numerics.cuh).
+// Row-complete epilogues (LayerNorm over N = hidden) run as a cluster of CLUSTER CTAs
+// along N; each CTA reduces its BN columns (an exact numpy subtree) and partial sums
+// are exchanged through DSMEM.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "numerics.cuh"
+#include "sm100.cuh"
+
+namespace samp {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_EPI_WARP0 = 2;
+
+__host__ __device__ constexpr int tmem_cols_for(int n) {
+  return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
+}
+
+template <int BN, int STAGES, int EPI_SMEM>
+struct GemmLayout {
+  static constexpr int A_BYTES = GEMM_BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int A_OFF = 0;
+  static constexpr int B_OFF = STAGES * A_BYTES;
+  static constexpr int BAR_OFF = B_OFF + STAGES * B_BYTES;
+  static constexpr int EPI_OFF = BAR_OFF + 8 * (2 * STAGES + 2) + 8;  // + tmem slot
+  static constexpr int EPI_OFF_ALIGNED = (EPI_OFF + 127) & ~127;
+  static constexpr int TOTAL = EPI_OFF_ALIGNED + EPI_SMEM + 1024;     // + alignment slack
+};
+
+// Shared epilogue context: where this thread's accumulator row lives.
+struct EpiCtx {
+  uint32_t taddr;    // TMEM address of (this thread's lane, column 0)
+  int row;           // global output row
+  int ep_tid;        // 0..127 (== tile row)
+  int n0;            // first output column of the tile
+  int M;             // valid rows
+};
+
+// Sum partials of the CLUSTER CTAs in numpy's tree order (each CTA holds one subtree).
+template <int CLUSTER>
+__device__ __forceinline__ float cluster_tree_sum(float* red, int ep_tid, float mine) {
+  if constexpr (CLUSTER == 1) {
+    return mine;
+  } else {
+    red[ep_tid] = mine;
+    cluster_sync_all();
+    float p[CLUSTER];
+#pragma unroll
+    for (int r = 0; r < CLUSTER; ++r) p[r] = dsmem_ld_f32(&red[ep_tid], r);
+    if constexpr (CLUSTER == 2) return __fadd_rn(p[0], p[1]);
+    else return __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
+  }
+}
+
+template <int KIND, int BN, int STAGES, int CLUSTER, class Epi>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+            int M, int k_bytes, const typename Epi::Params ep) {
+  using Lay = GemmLayout<BN, STAGES, Epi::SMEM_BYTES>;
+  constexpr int TMEM_COLS = tmem_cols_for(BN);
+  constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint8_t* epi_smem = smem + Lay::EPI_OFF_ALIGNED;
+
+  const uint32_t warp = warp_id();
+  const int m0 = blockIdx.y * GEMM_BM;
+  const int n0 = blockIdx.x * BN;
+  const int nk = k_bytes / 128;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp >= GEMM_EPI_WARP0) Epi::prologue(ep, epi_smem, threadIdx.x - GEMM_EPI_WARP0 * 32);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], Lay::A_BYTES + Lay::B_BYTES);
+        // coordinates are in elements: 128 bytes of K = 128 int8 or 64 f16
+        const int kc = KIND == KIND_I8 ? kb * 128 : kb * 64;
+        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kc, m0, &full[s]);
+        tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kc, n0, &full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&full[s], (kb / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_addr(smem + Lay::A_OFF + s * Lay::A_BYTES);
+        const uint32_t b_base = smem_addr(smem + Lay::B_OFF + s * Lay::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per 128B swizzle row
+          mma_ss<KIND>(tmem, sdesc_k_sw128(a_base + 32 * k), sdesc_k_sw128(b_base + 32 * k), IDESC,
+                       (kb | k) != 0);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    const int ep_tid = threadIdx.x - GEMM_EPI_WARP0 * 32;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int tile_row = quarter * 32 + lane_id();
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    EpiCtx c{tmem + (uint32_t(quarter * 32) << 16), m0 + tile_row, tile_row, n0, M};
+    (void)ep_tid;
+    Epi::template run<BN, CLUSTER>(ep, c, epi_smem);
+  }
+  // non-epilogue warps mirror the epilogue's cluster barriers
+  if (warp < GEMM_EPI_WARP0) {
+    for (int i = 0; i < Epi::template cluster_barriers<CLUSTER>(); ++i) cluster_sync_all();
+  }
+  if constexpr (CLUSTER > 1) cluster_sync_all();  // no CTA leaves while peers read its smem
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ epilogues
+
+// raw int32 / f32 accumulator store (kernel tests, parity of the accumulators)
+struct EpiStoreAcc {
+  struct Params {
+    void* out;   // int32 (kind::i8) or float (kind::f16), row-major
+    int ldc;     // elements
+  };
+  static constexpr int SMEM_BYTES = 0;
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
+  __device__ static void prologue(const Params&, uint8_t*, int) {}
+  template <int BN, int CLUSTER>
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t*) {
+#pragma unroll 1
+    for (int col = 0; col < BN; col += 32) {
+      uint32_t r[32];
+      tmem_ld32(c.taddr + col, r);
+      tmem_wait_ld();
+      if (c.row < c.M) {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint32_t*>(p.out) + size_t(c.row) * p.ldc + c.n0 + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
+  return (uint32_t(a) & 0xffu) | ((uint32_t(b) & 0xffu) << 8) | ((uint32_t(c) & 0xffu) << 16) |
+         ((uint32_t(d) & 0xffu) << 24);
+}
+
+// Fused QKV: per column block (q|k|v) dequant F32(acc)*F32(s_in*s_w) + bias, quantize
+// at the block's site (reference encoder.py:355-366).
+struct EpiQKV {
+  struct Params {
+    int8_t* out;          // [M][ldo]
+    int ldo;
+    const float* bias;    // [3H]
+    int block_cols;       // H
+    float mult[3];        // F32(double(s_in) * double(s_w{q,k,v}))
+    float s_out[3];       // F32(scale(L.attn.{q,k,v}))
+  };
+  static constexpr int SMEM_BYTES = 0;
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
+  __device__ static void prologue(const Params&, uint8_t*, int) {}
+  template <int BN, int CLUSTER>
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t*) {
+#pragma unroll 1
+    for (int col = 0; col < BN; col += 32) {
+      const int gcol = c.n0 + col;
+      const int blk = gcol / p.block_cols;
+      const float mult = p.mult[blk], so = p.s_out[blk];
+      uint32_t r[32];
+      tmem_ld32(c.taddr + col, r);
+      tmem_wait_ld();
+      uint32_t packed[8];
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + gcol + j));
+        int q0 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 0])), mult), b.x), so);
+        int q1 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 1])), mult), b.y), so);
+        int q2 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 2])), mult), b.z), so);
+        int q3 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 3])), mult), b.w), so);
+        packed[j / 4] = pack4_i8(q0, q1, q2, q3);
+      }
+      if (c.row < c.M) {
+        uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
+        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+    }
+  }
+};
+
+// FFN1: F32(acc)*mult + b1 -> GELU (numpy/SVML-exact) -> quantize(ffn.mid)
+// (reference encoder.py:406-410)
+struct EpiGeluQuant {
+  struct Params {
+    int8_t* out;
+    int ldo;
+    const float* bias;
+    float mult;
+    float s_out;
+  };
+  static constexpr int SMEM_BYTES = sizeof(TanhTable);
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
+  __device__ static void prologue(const Params&, uint8_t* smem, int tid) {
+    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, 128);
+  }
+  template <int BN, int CLUSTER>
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
+#pragma unroll 1
+    for (int col = 0; col < BN; col += 32) {
+      const int gcol = c.n0 + col;
+      uint32_t r[32];
+      tmem_ld32(c.taddr + col, r);
+      tmem_wait_ld();
+      uint32_t packed[8];
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + gcol + j));
+        const float bb[4] = {b.x, b.y, b.z, b.w};
+        int q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float mid = __fadd_rn(__fmul_rn(__int2float_rn(int(r[j + u])), p.mult), bb[u]);
+          q[u] = quant_i8(gelu_ref(mid, tt), p.s_out);
+        }
+        packed[j / 4] = pack4_i8(q[0], q[1], q[2], q[3]);
+      }
+      if (c.row < c.M) {
+        uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
+        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+    }
+  }
+};
+
+// Row-complete residual + LayerNorm epilogue (the paper's "big kernel"):
+//   x   = (F32(acc)*mult + bias) + residual      residual = F32(code)*s_in  or  f32
+//   out = ((x - mean) * inv) * gamma + beta      mean/var: numpy pairwise over H
+// then any of: int8 quantize(s_out), f32 store, f16 store.
+// (reference encoder.py:381-385 out-proj, :412-418 FFN2; kernels.layernorm :138-154)
+struct EpiResLN {
+  struct Params {
+    const float* bias;
+    const int8_t* res_i8;   // residual codes [M][H] (or null)
+    const float* res_f32;   // residual values [M][H] (or null)
+    float res_scale;
+    const float* gamma;
+    const float* beta;
+    float mult;             // int32 accumulator dequant multiplier
+    int acc_is_f32;         // kind::f16 GEMM: accumulator is already F32, no dequant
+    float eps;
+    int hidden;
+    int8_t* out_i8;  float s_out;   // optional
+    float* out_f32;                 // optional
+    __half* out_f16;                // optional
+  };
+  static constexpr int SMEM_BYTES = 2 * 128 * sizeof(float);
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return CLUSTER > 1 ? 2 : 0; }
+  __device__ static void prologue(const Params&, uint8_t*, int) {}
+
+  template <int BN, int CLUSTER>
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    float* red = reinterpret_cast<float*>(smem);
+    const bool valid = c.row < c.M;
+    const size_t rbase = size_t(valid ? c.row : 0) * p.hidden;
+    // pass 1: x = (acc*mult + b) + residual, written back into TMEM as f32 bits
+#pragma unroll 1
+    for (int col = 0; col < BN; col += 32) {
+      const int gcol = c.n0 + col;
+      uint32_t r[32];
+      tmem_ld32(c.taddr + col, r);
+      tmem_wait_ld();
+      float res[32];
+      if (p.res_i8) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.res_i8 + rbase + gcol);
+        uint4 u0 = src[0], u1 = src[1];
+        const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+        for (int j = 0; j < 32; ++j) res[j] = deq(int(int8_t((w[j / 4] >> (8 * (j % 4))) & 0xff)), p.res_scale);
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(p.res_f32 + rbase + gcol);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 v = src[j];
+          res[4 * j] = v.x; res[4 * j + 1] = v.y; res[4 * j + 2] = v.z; res[4 * j + 3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float b = __ldg(p.bias + gcol + j);
+        const float acc = p.acc_is_f32 ? __uint_as_float(r[j]) : __fmul_rn(__int2float_rn(int(r[j])), p.mult);
+        r[j] = __float_as_uint(__fadd_rn(__fadd_rn(acc, b), res[j]));
+      }
+      tmem_st32(c.taddr + col, r);
+    }
+    tmem_wait_st();
+
+    auto get_x = [&](int off, float (&v)[8]) {
+      uint32_t u[8];
+      tmem_ld8(c.taddr + off, u);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(u[j]);
+    };
+    float s1 = pairwise_sum(BN, get_x);
+    float total = cluster_tree_sum<CLUSTER>(red, c.ep_tid, s1);
+    const float hf = float(p.hidden);
+    const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
+
+    auto get_c2 = [&](int off, float (&v)[8]) {
+      uint32_t u[8];
+      tmem_ld8(c.taddr + off, u);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float d = __fsub_rn(__uint_as_float(u[j]), mean);
+        v[j] = __fmul_rn(d, d);
+      }
+    };
+    float s2 = pairwise_sum(BN, get_c2);
+    float total2 = cluster_tree_sum<CLUSTER>(red + 128, c.ep_tid, s2);
+    const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+
+    // pass 3: normalise, affine, emit
+#pragma unroll 1
+    for (int col = 0; col < BN; col += 32) {
+      const int gcol = c.n0 + col;
+      uint32_t r[32];
+      tmem_ld32(c.taddr + col, r);
+      tmem_wait_ld();
+      float y[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float g = __ldg(p.gamma + gcol + j), b = __ldg(p.beta + gcol + j);
+        y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(__uint_as_float(r[j]), mean), inv), g), b);
+      }
+      if (!valid) continue;
+      if (p.out_i8) {
+        uint32_t packed[8];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          packed[j / 4] = pack4_i8(quant_i8(y[j], p.s_out), quant_i8(y[j + 1], p.s_out),
+                                   quant_i8(y[j + 2], p.s_out), quant_i8(y[j + 3], p.s_out));
+        uint4* dst = reinterpret_cast<uint4*>(p.out_i8 + rbase + gcol);
+        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+      if (p.out_f32) {
+        float4* dst = reinterpret_cast<float4*>(p.out_f32 + rbase + gcol);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+      }
+      if (p.out_f16) {
+        uint4* dst = reinterpret_cast<uint4*>(p.out_f16 + rbase + gcol);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __half2 h0 = __floats2half2_rn(y[8 * j], y[8 * j + 1]), h1 = __floats2half2_rn(y[8 * j + 2], y[8 * j + 3]);
+          __half2 h2 = __floats2half2_rn(y[8 * j + 4], y[8 * j + 5]), h3 = __floats2half2_rn(y[8 * j + 6], y[8 * j + 7]);
+          dst[j] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                              *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+        }
+      }
+    }
+  }
+};
+
+}  // namespace samp
+
+// ------------------------------------------------------------------ host launcher
+namespace samp {
+
+template <int KIND, int BN, int STAGES, int CLUSTER, class Epi>
+inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N, int k_bytes,
+                               const typename Epi::Params& p, cudaStream_t stream) {
+  using Lay = GemmLayout<BN, STAGES, Epi::SMEM_BYTES>;
+  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, Epi>;
+  static thread_local int configured_device = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_device != dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured_device = dev;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, 1);
+  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Lay::TOTAL;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  cfg.numAttrs = 0;
+  if (CLUSTER > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, map_a, map_b, M, k_bytes, p);
+}
+
+}  // namespace samp

@@ -1,0 +1,394 @@
+"""Benchmark: BERT-base seq-128 sentences/s on B200 (BASELINE.json metric, configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl samp_b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+Workload (``value``): BERT-base (12L, H768, random init seed 0, weight_scale 0.02),
+fully-quantized INT8 plan (12/12 layers), classification head, batch 32 x seq 128
+synthetic token ids per GPU, inputs resident in HBM.  Each timed step is one full
+forward of the batch; L2 is flushed (256 MiB write) before every timed step; steps
+are timed with CUDA events on the launching stream and the job time is the max over
+ranks.  Weak scaling: every rank runs its own 32 sentences (independent replicas,
+no collective on the data path).
+
+``e2e``: the same batch through the public API (``Engine.forward_packed``) with host
+arrays: H2D of ids/segments and D2H of logits/probs/labels inside the timed region.
+
+``--impl reference``: the reference's own CPU path (the oracle port of
+pkg/src/samp/encoder.py, same weights and calibration) timed on this host's cores,
+each step a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODEL = "bert-base"
+BATCH, SEQ = 32, 128
+METRIC = "BERT-base seq128 sentences/s (1/2/4/8 B200) & batch-1 p50 latency per mode"
+CALIB = os.path.join(ROOT, "tests", "golden", f"bench_calibration_{MODEL}.json")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "dram_traffic.json")
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_model():
+    from paper_2209_09130_b200.quantization import CalibrationTable
+    from paper_2209_09130_b200.synthetic import bert_archive
+
+    arch = bert_archive(MODEL, task="classification", num_labels=2, seed=0, weight_scale=0.02)
+    with open(CALIB) as fh:
+        table = CalibrationTable.from_json(fh.read())
+    if table.model_fingerprint != arch.fingerprint:
+        raise RuntimeError("bench calibration does not belong to the bench archive (fingerprint mismatch)")
+    arch.calibration = table
+    return arch
+
+
+def synthetic_batch(rank: int, batch: int = BATCH, seq: int = SEQ):
+    """cli._random_inputs recipe (reference cli.py:333-341): default_rng ids, segment 0, no padding."""
+    rng = np.random.default_rng(rank)
+    ids = rng.integers(0, 30522, size=(batch, seq)).astype(np.int32).reshape(-1)
+    segs = np.zeros(batch * seq, np.int32)
+    seq_start = (np.arange(batch + 1) * seq).astype(np.int32)
+    att = np.full(batch, seq, np.int32)
+    return seq_start, att, ids, segs
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gemm_ops(T: int, H: int, I: int) -> dict:
+    """Algorithmic INT8 ops (2 per MAC) per launch of each kernel over T tokens."""
+    return {"qkv_i8": 2 * T * H * 3 * H, "outproj_i8": 2 * T * H * H, "ffn1_i8": 2 * T * H * I,
+            "ffn2_i8": 2 * T * I * H, "qkv_f16": 2 * T * H * 3 * H, "outproj_f16": 2 * T * H * H,
+            "ffn1_f16": 2 * T * H * I, "ffn2_f16": 2 * T * I * H}
+
+
+def run_samp(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2209_09130_b200 import _lib
+    from paper_2209_09130_b200.engine import HEAD_CLASSIFY, IO_DEVICE, Engine
+    from paper_2209_09130_b200.plan import PrecisionPlan
+
+    arch = build_model()
+    eng = Engine(arch, device=local)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
+    seq_start, att, ids, segs = synthetic_batch(rank)
+    T = int(seq_start[-1])
+    d_ids = torch.from_numpy(ids).to(dev)
+    d_segs = torch.from_numpy(segs).to(dev)
+    nl = arch.manifest.num_labels
+    d_logits = torch.empty((BATCH, nl), dtype=torch.float32, device=dev)
+    d_probs = torch.empty_like(d_logits)
+    d_labels = torch.empty(BATCH, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lib = _lib.load()
+    out = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), HEAD_CLASSIFY)
+    codes = plan.codes()
+
+    def fwd(p=codes):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(lib.samp_forward(eng.handle, p, BATCH, seq_start.ctypes.data, att.ctypes.data,
+                                    d_ids.data_ptr(), d_segs.data_ptr(), IO_DEVICE, out, st))
+
+    def timed_steps(n, fn, flush_l2=True):
+        tot = 0.0
+        for _ in range(n):
+            if flush_l2:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        return tot
+
+    for _ in range(args.warmup):
+        fwd()
+    torch.cuda.synchronize()
+    launches = eng.last_launch_count()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    gpu_id = str(getattr(torch.cuda.get_device_properties(dev), "uuid", local))
+    if gpu_id and not gpu_id.startswith("GPU-") and len(gpu_id) > 8:
+        gpu_id = "GPU-" + gpu_id
+    barrier()
+    with ClockSampler(gpu_id) as clocks:
+        ms = timed_steps(args.steps, fwd)
+    barrier()
+    job_ms = max_over_ranks(ms)
+    value = world * BATCH * args.steps / (job_ms / 1e3)
+
+    # ---------------- e2e through the public API with host buffers
+    barrier()
+    e2e_ms = 0.0
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = eng.forward_packed(plan, seq_start, att, ids, segs, hidden=False)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_ms += (t1 - t0) * 1e3
+        assert res.labels is not None
+    e2e_ms = max_over_ranks(e2e_ms)
+    e2e = {"value": world * BATCH * args.steps / (e2e_ms / 1e3), "unit": "sentences/s",
+           "h2d_bytes_per_step": int(ids.nbytes + segs.nbytes),
+           "d2h_bytes_per_step": int(BATCH * nl * 4 * 2 + BATCH * 4)}
+
+    # ---------------- per-kernel device times (separate pass, CUDA events per launch)
+    _lib.check(lib.samp_set_profiling(eng.handle, 1))
+    timed_steps(args.steps, fwd)
+    buf = (__import__("ctypes").create_string_buffer(1 << 16))
+    _lib.check(lib.samp_profile_report(eng.handle, buf, len(buf)))
+    _lib.check(lib.samp_set_profiling(eng.handle, 0))
+    prof = json.loads(buf.value.decode())
+    H, I = arch.manifest.hidden, arch.manifest.intermediate
+    ops = gemm_ops(T, H, I)
+    ops["attention_i8"] = 4 * BATCH * SEQ * SEQ * H
+    kernels = {}
+    for name, (tot_ms, n) in prof.items():
+        avg = tot_ms / n
+        rec = {"avg_us": round(avg * 1e3, 2), "launches": n, "share": None}
+        if name in ops:
+            rec["achieved_tops"] = round(ops[name] / (avg * 1e-3) / 1e12, 1)
+        kernels[name] = rec
+    total = sum(v[0] for v in prof.values())
+    for name, (tot_ms, _) in prof.items():
+        kernels[name]["share"] = round(tot_ms / total, 4)
+    dom = max((k for k in prof if k in ops), key=lambda k: prof[k][0])
+    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+    bf16 = peaks.get("bf16_tflops_sustained")
+    peak_src = "2 x MEASURED_PEAKS.bf16_tflops_sustained (B200 dense int8 = 2 x dense bf16)"
+    if bf16 is None:
+        bf16, peak_src = 1400.0, "2 x fallback 1.4 PFLOP/s sustained bf16 (B200_PROFILING.md)"
+    peak = 2.0 * bf16
+    achieved = kernels[dom]["achieved_tops"]
+    traffic = None
+    if os.path.exists(TRAFFIC):
+        traffic = json.load(open(TRAFFIC)).get(dom)
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "ops_per_launch": ops[dom]}
+
+    # ---------------- batch-1 p50 latency per mode (device time, L2 flushed)
+    lat = {}
+    b1_start, b1_att = np.array([0, SEQ], np.int32), np.array([SEQ], np.int32)
+    out1 = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), HEAD_CLASSIFY)
+    for label, mode, k in (("fp16", "FP", 0), ("ffn-only-12", "FFN_ONLY", L), ("fully-quant-12", "FULLY_QUANT", L)):
+        pc = PrecisionPlan.prefix(mode, L, k).codes()
+
+        def one(pc=pc):
+            st = torch.cuda.current_stream(dev).cuda_stream
+            _lib.check(lib.samp_forward(eng.handle, pc, 1, b1_start.ctypes.data, b1_att.ctypes.data,
+                                        d_ids.data_ptr(), d_segs.data_ptr(), IO_DEVICE, out1, st))
+        for _ in range(3):
+            one()
+        samples = []
+        for _ in range(args.lat_iters):
+            samples.append(timed_steps(1, one))
+        lat[label] = round(statistics.median(samples), 4)
+    # restore the batch geometry cache for any later call
+    barrier()
+
+    line = None
+    if rank == 0:
+        cpu = cpu_baseline(arch, plan, args) if (world == 1 and not args.no_cpu) else None
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "sentences/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (random ids, random-init weights seed 0; reference-calibrated scales)",
+            "config": {"workload": "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 per GPU (configs[1])",
+                       "model": MODEL, "plan": "FULLY_QUANT k=12", "batch_per_gpu": BATCH, "seq_len": SEQ,
+                       "global_batch": BATCH * world, "parallelism": f"replicas x{world} (batch-sharded)",
+                       "l2": "flushed before every timed step (256 MiB write)"},
+            "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
+            "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps,
+            "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((d.get("num_threads", 1) for d in info), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(arch, plan, args, n_sent=None):
+    """The reference's CPU path (oracle port) on a bounded sample of the same workload."""
+    from oracle import samp_oracle as orc
+
+    n_sent = n_sent or args.cpu_sentences
+    amax = {s: e.amax for s, e in arch.calibration.entries.items()}
+    model = orc.Model.from_manifest(arch.manifest, arch.tensors, amax)
+    seq_start, att, ids, segs = synthetic_batch(0)
+    model.qlayer(0)  # weight quantization is load-time in the reference (cached), keep it out
+    for i in range(arch.manifest.num_layers):
+        model.qlayer(i)
+    t0 = time.perf_counter()
+    for s in range(n_sent):
+        r0, r1 = seq_start[s], seq_start[s + 1]
+        h = orc.run(model, ids[r0:r1], segs[r0:r1], int(att[s]), plan.layer_precisions)
+        orc.classify_logits(model, h)
+    dt = time.perf_counter() - t0
+    return {"value": round(n_sent / dt, 4), "unit": "sentences/s", "cores": _blas_threads(), "kind": "port",
+            "sample": f"{n_sent} of the 32 x 128-token sentences, FULLY_QUANT 12/12 + classify head, "
+                      f"oracle port of the reference (numpy, OpenBLAS threads for the int8 GEMMs)"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    from paper_2209_09130_b200.plan import PrecisionPlan
+
+    arch = build_model()
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
+    n = args.ref_sentences
+    for _ in range(args.warmup):
+        cpu_baseline(arch, plan, args, n_sent=1)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = cpu_baseline(arch, plan, args, n_sent=n)
+        t_all += time.perf_counter() - t0
+        vals.append(r["value"])
+    value = n * args.steps / t_all
+    line = {
+        "metric": METRIC, "impl": "reference", "value": round(value, 4), "unit": "sentences/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_all * 1e3 / args.steps, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 (configs[1])",
+                   "model": MODEL, "plan": "FULLY_QUANT k=12", "step_sample": f"{n} sentences of the batch"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "sentences/s", "cores": _blas_threads(),
+                         "kind": "port", "sample": f"{n} x 128-token sentences per step"},
+        "e2e": {"value": round(value, 4), "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="samp_b200", choices=["samp_b200", "reference"])
+    ap.add_argument("--lat-iters", type=int, default=30)
+    ap.add_argument("--cpu-sentences", type=int, default=12)
+    ap.add_argument("--ref-sentences", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_samp(args)
+
+
+if __name__ == "__main__":
+    main()

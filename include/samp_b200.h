@@ -115,8 +115,21 @@ int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, siz
 int samp_debug_gemm_i8(const int8_t* a, const int8_t* b, int32_t* c, int m, int n, int k);
 int samp_debug_gemm_f16(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);
 
+/* numerics validation: exhaustive (all 2^32 inputs) comparisons of the branch-free
+ * quantize / divide / exp used by the kernels against their IEEE-divide formulations,
+ * and device evaluation of fn 0 = numpy exp, 1 = numpy (SVML) tanh, 2 = reference GELU */
+int samp_debug_quant_exhaustive(const float* scales, int n, unsigned long long* mismatches);
+int samp_debug_div_exhaustive(const float* divisors, int n, unsigned long long* mismatches);
+int samp_debug_exp_exhaustive(unsigned long long* mismatches);
+int samp_debug_unary(int fn, const float* x, float* y, long n);
+
 /* number of kernel launches issued by the last samp_forward (for bench gpu_launches) */
 int samp_last_launch_count(samp_engine* e);
+
+/* per-kernel device timing: with profiling on, every launch is bracketed by CUDA events
+ * on the engine stream; samp_profile_report syncs and writes {"kernel": [total_ms, n], ...} */
+int samp_set_profiling(samp_engine* e, int on);
+int samp_profile_report(samp_engine* e, char* buf, size_t cap);
 
 #ifdef __cplusplus
 }

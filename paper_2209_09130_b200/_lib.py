@@ -65,7 +65,13 @@ SIGNATURES = [
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("samp_debug_gemm_f16", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("samp_debug_quant_exhaustive", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
+    ("samp_debug_div_exhaustive", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
+    ("samp_debug_exp_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
+    ("samp_debug_unary", ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long]),
     ("samp_last_launch_count", ctypes.c_int, [ctypes.c_void_p]),
+    ("samp_set_profiling", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    ("samp_profile_report", ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
 ]
 
 _lib = None

@@ -62,10 +62,10 @@ static void debug_gemm(const void* a, const void* b, void* c, int m, int n, int 
   const int kb = k * eb;
   cudaError_t e;
   switch (bn) {
-    case 256: e = launch_gemm<KIND, 256, 4, 1, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
-    case 128: e = launch_gemm<KIND, 128, 4, 1, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
-    case 64: e = launch_gemm<KIND, 64, 4, 1, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
-    default: e = launch_gemm<KIND, 32, 4, 1, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
+    case 256: e = launch_gemm<KIND, 256, 4, 1, 4, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
+    case 128: e = launch_gemm<KIND, 128, 4, 1, 4, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
+    case 64: e = launch_gemm<KIND, 64, 4, 1, 4, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
+    default: e = launch_gemm<KIND, 32, 4, 1, 4, EpiStoreAcc>(ma, mb, m, n, kb, p, 0); break;
   }
   SAMP_CUDA(e);
   SAMP_CUDA(cudaDeviceSynchronize());

@@ -1,0 +1,140 @@
+// Numerics validation entry points (tests only): the branch-free quantize / divide used
+// by every epilogue against the IEEE-divide formulation, exhaustively over all 2^32
+// float bit patterns, and device evaluation of exp / tanh / GELU for oracle comparison.
+#include "host_util.h"
+#include "numerics.cuh"
+
+namespace samp {
+
+__device__ __forceinline__ float np_expf_ieee(float x) {  // np_expf with __fdiv_rn
+  if (!(x < 88.72283935546875f)) return x != x ? x : __int_as_float(0x7f800000);
+  if (x <= -103.97208404541015625f) return 0.0f;
+  const float magic = 12582912.0f;
+  float k = __fmul_rn(x, 1.442695040888963407359924681001892137f);
+  k = __fsub_rn(__fadd_rn(k, magic), magic);
+  float r = __fmaf_rn(k, -6.93145752e-1f, x);
+  r = __fmaf_rn(k, -1.42860677e-6f, r);
+  r = __fmaf_rn(k, 0.0f, r);
+  float num = __fmaf_rn(5.082762527590693718096e-04f, r, 6.757896990527504603057e-03f);
+  num = __fmaf_rn(num, r, 5.114512081637298353406e-02f);
+  num = __fmaf_rn(num, r, 2.473615434895520810817e-01f);
+  num = __fmaf_rn(num, r, 7.257664613233124478488e-01f);
+  num = __fmaf_rn(num, r, 9.999999999980870924916e-01f);
+  float den = __fmaf_rn(2.159509375685829852307e-02f, r, -2.742335390411667452936e-01f);
+  den = __fmaf_rn(den, r, 1.0f);
+  return scale_pow2(__fdiv_rn(num, den), static_cast<int>(k));
+}
+
+__global__ void quant_exhaustive_kernel(const float* scales, int n, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (int si = 0; si < n; ++si) {
+    const float s = scales[si];
+    const Recip r = make_recip(s);
+    for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < (1ull << 32);
+         u += uint64_t(gridDim.x) * blockDim.x) {
+      const float x = __uint_as_float(uint32_t(u));
+      if (x != x) continue;  // NaN codes are unspecified in the reference (clip keeps NaN)
+      local += quant_fast(x, r) != quant_i8(x, s);
+    }
+  }
+  atomicAdd(bad, local);
+}
+
+__global__ void div_exhaustive_kernel(const float* divisors, int n, unsigned long long* bad) {
+  // quotient identity over the operand ranges the kernels use it for: x in [0, 1] (softmax
+  // numerators) and any normal x with |x| in [2^-60, 2^60]
+  unsigned long long local = 0;
+  for (int si = 0; si < n; ++si) {
+    const Recip r = make_recip(divisors[si]);
+    for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < (1ull << 32);
+         u += uint64_t(gridDim.x) * blockDim.x) {
+      const float x = __uint_as_float(uint32_t(u));
+      const float ax = fabsf(x);
+      if (!(ax >= 8.6736174e-19f && ax <= 1.1529215e18f)) continue;
+      const float a = div_fast(x, r), b = __fdiv_rn(x, divisors[si]);
+      local += __float_as_uint(a) != __float_as_uint(b);
+    }
+  }
+  atomicAdd(bad, local);
+}
+
+__global__ void exp_exhaustive_kernel(unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < (1ull << 32);
+       u += uint64_t(gridDim.x) * blockDim.x) {
+    const float x = __uint_as_float(uint32_t(u));
+    const float a = np_expf(x), b = np_expf_ieee(x);
+    local += (__float_as_uint(a) != __float_as_uint(b)) && !(a != a && b != b);
+  }
+  atomicAdd(bad, local);
+}
+
+__global__ void unary_kernel(int fn, const float* x, float* y, long n) {
+  __shared__ TanhTable tt;
+  load_tanh_table(&tt, threadIdx.x, blockDim.x);
+  __syncthreads();
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    y[i] = fn == 0 ? np_expf(v) : fn == 1 ? np_tanhf(v, &tt) : gelu_ref(v, &tt);
+  }
+}
+
+static unsigned long long run_count(void (*launch)(unsigned long long*)) {
+  unsigned long long* d;
+  SAMP_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  SAMP_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+  launch(d);
+  SAMP_CUDA(cudaGetLastError());
+  SAMP_CUDA(cudaDeviceSynchronize());
+  unsigned long long h = 0;
+  SAMP_CUDA(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return h;
+}
+
+static float* g_vals = nullptr;
+static int g_n = 0;
+
+}  // namespace samp
+
+using namespace samp;
+
+extern "C" int samp_debug_quant_exhaustive(const float* scales, int n, unsigned long long* mismatches) {
+  return guarded([&] {
+    SAMP_CUDA(cudaMalloc(&g_vals, n * sizeof(float)));
+    SAMP_CUDA(cudaMemcpy(g_vals, scales, n * sizeof(float), cudaMemcpyHostToDevice));
+    g_n = n;
+    *mismatches = run_count([](unsigned long long* d) { quant_exhaustive_kernel<<<148 * 8, 256>>>(g_vals, g_n, d); });
+    cudaFree(g_vals);
+  });
+}
+
+extern "C" int samp_debug_div_exhaustive(const float* divisors, int n, unsigned long long* mismatches) {
+  return guarded([&] {
+    SAMP_CUDA(cudaMalloc(&g_vals, n * sizeof(float)));
+    SAMP_CUDA(cudaMemcpy(g_vals, divisors, n * sizeof(float), cudaMemcpyHostToDevice));
+    g_n = n;
+    *mismatches = run_count([](unsigned long long* d) { div_exhaustive_kernel<<<148 * 8, 256>>>(g_vals, g_n, d); });
+    cudaFree(g_vals);
+  });
+}
+
+extern "C" int samp_debug_exp_exhaustive(unsigned long long* mismatches) {
+  return guarded([&] {
+    *mismatches = run_count([](unsigned long long* d) { exp_exhaustive_kernel<<<148 * 8, 256>>>(d); });
+  });
+}
+
+extern "C" int samp_debug_unary(int fn, const float* x, float* y, long n) {
+  return guarded([&] {
+    float *dx, *dy;
+    SAMP_CUDA(cudaMalloc(&dx, n * 4));
+    SAMP_CUDA(cudaMalloc(&dy, n * 4));
+    SAMP_CUDA(cudaMemcpy(dx, x, n * 4, cudaMemcpyHostToDevice));
+    unary_kernel<<<148 * 4, 256>>>(fn, dx, dy, n);
+    SAMP_CUDA(cudaGetLastError());
+    SAMP_CUDA(cudaMemcpy(y, dy, n * 4, cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dy);
+  });
+}

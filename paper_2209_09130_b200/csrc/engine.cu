@@ -1,0 +1,811 @@
+// The samp_b200 engine: device weights, calibration scales, activation buffers and
+// the per-layer mixed-precision forward (reference Engine, pkg/src/samp/encoder.py:421-530).
+//
+// Per-layer kernel sequence (5 launches per layer + embed + head):
+//   FULL_INT8  QKV i8 GEMM [dequant+bias+quantize q|k|v] -> attention i8 ->
+//              out-proj i8 GEMM [dequant+bias+residual+LN+quantize ffn.in] ->
+//              FFN1 i8 GEMM [dequant+bias+GELU+quantize ffn.mid] ->
+//              FFN2 i8 GEMM [dequant+bias+residual+LN (+quantize next attn.in | f32)]
+//   FFN_ONLY   QKV f16 GEMM -> attention f16 -> out-proj f16 GEMM [+LN+quantize ffn.in] ->
+//              FFN1 i8 -> FFN2 i8
+//   FP         f16 GEMMs/attention, LN epilogues in F32 (f16 storage)
+//   MHA_ONLY   (extension) INT8 attention block, FP16 FFN on dequantized ffn.in codes
+// No standalone quantize / dequantize / LayerNorm kernel exists: every one is fused.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "host_util.h"
+#include "kernels.h"
+
+namespace samp {
+
+// ------------------------------------------------------------------ helpers
+static double site_scale(double amax) { return std::max(amax, 127 * 1e-8) / 127.0; }
+static float f32(double x) { return static_cast<float>(x); }
+static float mult_of(double a, double b) { return static_cast<float>(a * b); }
+
+static double host_amax(const float* w, size_t n) {
+  float m = 0.0f;
+  for (size_t i = 0; i < n; ++i) m = std::max(m, std::fabs(w[i]));
+  return double(m);
+}
+
+struct DevMem {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    SAMP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void release(void* p) {
+    for (auto& q : ptrs)
+      if (q == p) {
+        cudaFree(q);
+        q = nullptr;
+      }
+  }
+  ~DevMem() {
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+struct LayerDev {
+  bool loaded = false;
+  int8_t *qkv_i8 = nullptr, *wo_i8 = nullptr, *w1_i8 = nullptr, *w2_i8 = nullptr;    // K-major
+  __half *qkv_f16 = nullptr, *wo_f16 = nullptr, *w1_f16 = nullptr, *w2_f16 = nullptr;
+  float *qkv_b = nullptr, *ob = nullptr, *ln1_g = nullptr, *ln1_b = nullptr;
+  float *b1 = nullptr, *b2 = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
+  double s_w[6] = {0, 0, 0, 0, 0, 0};  // qw kw vw ow w1 w2
+  CUtensorMap m_qkv_i8, m_wo_i8, m_w1_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w1_f16, m_w2_f16;
+};
+
+static int pick_bn(int n) {
+  for (int bn : {256, 128, 64})
+    if (n % bn == 0) return bn;
+  return 0;
+}
+
+static Tiles choose_tiles(int H, int I) {
+  Tiles t{};
+  t.bn_qkv = pick_bn(H);
+  t.bn_ffn1 = pick_bn(I);
+  const int cand[][2] = {{192, 4}, {256, 4}, {256, 2}, {192, 2}, {256, 1}, {128, 1}, {64, 1}};
+  for (auto& c : cand)
+    if (c[0] * c[1] == H && pw_splits_evenly(H, c[1])) {
+      t.bn_ln = c[0];
+      t.cluster_ln = c[1];
+      break;
+    }
+  return t;
+}
+
+// ------------------------------------------------------------------ engine
+struct Activations {
+  int cap = 0;  // token rows
+  float *hid_f32 = nullptr, *ln1_f32 = nullptr;
+  __half *hid_f16 = nullptr, *qkv_f16 = nullptr, *ctx_f16 = nullptr, *ln1_f16 = nullptr, *mid_f16 = nullptr;
+  int8_t *xq[2] = {nullptr, nullptr}, *qkv_i8 = nullptr, *ctx_i8 = nullptr, *ffn_in_i8 = nullptr, *mid_i8 = nullptr;
+  int *ids = nullptr, *segs = nullptr, *pos = nullptr;
+  float *logits = nullptr, *probs = nullptr, *pooled = nullptr;
+  int* labels = nullptr;
+  // A-operand tensor maps (box 128 B x 128 rows) and attention maps (box one head row x 64 rows)
+  CUtensorMap a_xq[2], a_ctx_i8, a_ffn_in, a_mid_i8, a_hid_f16, a_ctx_f16, a_ln1_f16, a_mid_f16;
+  CUtensorMap att_qkv_i8, att_qkv_f16;
+};
+
+struct Geometry {
+  std::vector<int> seq_start, att_len, tile_seq, tile_q0;
+  int nseq = 0, T = 0, ntiles = 0, max_nkp = 0;
+  int *d_seq_start = nullptr, *d_att_len = nullptr, *d_tile_seq = nullptr, *d_tile_q0 = nullptr;
+  int cap_seq = 0, cap_tiles = 0;
+};
+
+}  // namespace samp
+
+struct samp_engine {
+  samp_model_desc d{};
+  int device = 0;
+  cudaStream_t stream = nullptr;          // the engine's own stream
+  cudaStream_t stream_in_use = nullptr;   // stream of the current samp_forward
+  samp::Tiles tiles{};
+  samp::DevMem mem;
+  // embeddings + heads (F32)
+  float *word = nullptr, *position = nullptr, *token_type = nullptr, *emb_g = nullptr, *emb_b = nullptr;
+  float *pool_w = nullptr, *pool_b = nullptr, *head_wt = nullptr, *head_b = nullptr;
+  bool emb_loaded = false, heads_loaded = false;
+  std::vector<samp::LayerDev> layers;
+  std::map<std::string, double> amax;
+  samp::Activations act;
+  samp::Geometry geo;
+  int launches = 0;
+  bool capture = false;
+  std::map<std::string, std::vector<uint8_t>> stages;
+  std::vector<int> h_pos;
+  bool profiling = false;
+  struct Pending { std::string name; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, std::pair<double, long>> prof;  // name -> (total ms, launches)
+  int* pinned_ids = nullptr;   // staging for host inputs
+  int pinned_cap = 0;
+};
+
+namespace samp {
+
+static void ensure_activations(samp_engine* e, int T) {
+  Activations& a = e->act;
+  if (T <= a.cap) return;
+  int cap = std::max(T, 256);
+  cap = (cap + 127) / 128 * 128;
+  const int H = e->d.hidden, I = e->d.intermediate, L = std::max(1, e->d.num_labels);
+  auto drop = [&](void* p) {
+    if (p) e->mem.release(p);
+  };
+  drop(a.hid_f32); drop(a.ln1_f32); drop(a.hid_f16); drop(a.qkv_f16); drop(a.ctx_f16); drop(a.ln1_f16);
+  drop(a.mid_f16); drop(a.xq[0]); drop(a.xq[1]); drop(a.qkv_i8); drop(a.ctx_i8); drop(a.ffn_in_i8);
+  drop(a.mid_i8); drop(a.ids); drop(a.segs); drop(a.pos); drop(a.logits); drop(a.probs); drop(a.labels); drop(a.pooled);
+  a.hid_f32 = e->mem.alloc<float>(size_t(cap) * H);
+  a.ln1_f32 = e->mem.alloc<float>(size_t(cap) * H);
+  a.hid_f16 = e->mem.alloc<__half>(size_t(cap) * H);
+  a.qkv_f16 = e->mem.alloc<__half>(size_t(cap) * 3 * H);
+  a.ctx_f16 = e->mem.alloc<__half>(size_t(cap) * H);
+  a.ln1_f16 = e->mem.alloc<__half>(size_t(cap) * H);
+  a.mid_f16 = e->mem.alloc<__half>(size_t(cap) * I);
+  a.xq[0] = e->mem.alloc<int8_t>(size_t(cap) * H);
+  a.xq[1] = e->mem.alloc<int8_t>(size_t(cap) * H);
+  a.qkv_i8 = e->mem.alloc<int8_t>(size_t(cap) * 3 * H);
+  a.ctx_i8 = e->mem.alloc<int8_t>(size_t(cap) * H);
+  a.ffn_in_i8 = e->mem.alloc<int8_t>(size_t(cap) * H);
+  a.mid_i8 = e->mem.alloc<int8_t>(size_t(cap) * I);
+  a.ids = e->mem.alloc<int>(cap);
+  a.segs = e->mem.alloc<int>(cap);
+  a.pos = e->mem.alloc<int>(cap);
+  a.logits = e->mem.alloc<float>(size_t(cap) * L);
+  a.probs = e->mem.alloc<float>(size_t(cap) * L);
+  a.labels = e->mem.alloc<int>(cap);
+  a.pooled = e->mem.alloc<float>(size_t(cap) * H);
+  a.cap = cap;
+  // GEMM A operands: K-major rows, 128-byte boxes, 128 rows
+  a.a_xq[0] = tmap_i8(a.xq[0], cap, H, H, 128, 128);
+  a.a_xq[1] = tmap_i8(a.xq[1], cap, H, H, 128, 128);
+  a.a_ctx_i8 = tmap_i8(a.ctx_i8, cap, H, H, 128, 128);
+  a.a_ffn_in = tmap_i8(a.ffn_in_i8, cap, H, H, 128, 128);
+  a.a_mid_i8 = tmap_i8(a.mid_i8, cap, I, I, 128, 128);
+  a.a_hid_f16 = tmap_f16(a.hid_f16, cap, H, H, 64, 128);
+  a.a_ctx_f16 = tmap_f16(a.ctx_f16, cap, H, H, 64, 128);
+  a.a_ln1_f16 = tmap_f16(a.ln1_f16, cap, H, H, 64, 128);
+  a.a_mid_f16 = tmap_f16(a.mid_f16, cap, I, I, 64, 128);
+  // attention: one head row (64 int8 / 64 f16) x 64 rows
+  a.att_qkv_i8 = tmap_i8(a.qkv_i8, cap, 3 * H, 3 * H, 64, 64, CU_TENSOR_MAP_SWIZZLE_64B);
+  a.att_qkv_f16 = tmap_f16(a.qkv_f16, cap, 3 * H, 3 * H, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, const int32_t* att_len) {
+  Geometry& g = e->geo;
+  const bool same = g.nseq == nseq && std::equal(seq_start, seq_start + nseq + 1, g.seq_start.begin()) &&
+                    std::equal(att_len, att_len + nseq, g.att_len.begin());
+  if (same && g.nseq > 0) return;
+  g.nseq = nseq;
+  g.seq_start.assign(seq_start, seq_start + nseq + 1);
+  g.att_len.resize(nseq);
+  g.tile_seq.clear();
+  g.tile_q0.clear();
+  g.max_nkp = 0;
+  e->h_pos.resize(seq_start[nseq]);
+  for (int s = 0; s < nseq; ++s) {
+    const int S = seq_start[s + 1] - seq_start[s];
+    g.att_len[s] = std::min(att_len[s], S);
+    for (int q = 0; q < S; q += 128) {
+      g.tile_seq.push_back(s);
+      g.tile_q0.push_back(q);
+    }
+    for (int t = 0; t < S; ++t) e->h_pos[seq_start[s] + t] = t;
+    g.max_nkp = std::max(g.max_nkp, (S + 31) & ~31);
+  }
+  g.T = seq_start[nseq];
+  g.ntiles = int(g.tile_seq.size());
+  if (nseq + 1 > g.cap_seq) {
+    if (g.d_seq_start) { e->mem.release(g.d_seq_start); e->mem.release(g.d_att_len); }
+    g.cap_seq = std::max(nseq + 1, 64);
+    g.d_seq_start = e->mem.alloc<int>(g.cap_seq);
+    g.d_att_len = e->mem.alloc<int>(g.cap_seq);
+  }
+  if (g.ntiles > g.cap_tiles) {
+    if (g.d_tile_seq) { e->mem.release(g.d_tile_seq); e->mem.release(g.d_tile_q0); }
+    g.cap_tiles = std::max(g.ntiles, 64);
+    g.d_tile_seq = e->mem.alloc<int>(g.cap_tiles);
+    g.d_tile_q0 = e->mem.alloc<int>(g.cap_tiles);
+  }
+  ensure_activations(e, g.T);
+  SAMP_CUDA(cudaMemcpyAsync(g.d_seq_start, g.seq_start.data(), (nseq + 1) * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaMemcpyAsync(g.d_att_len, g.att_len.data(), nseq * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaMemcpyAsync(g.d_tile_seq, g.tile_seq.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaMemcpyAsync(g.d_tile_q0, g.tile_q0.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaMemcpyAsync(e->act.pos, e->h_pos.data(), g.T * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));  // host vectors may change on the next call
+}
+
+static double need_amax(samp_engine* e, const std::string& site) {
+  auto it = e->amax.find(site);
+  SAMP_REQUIRE(it != e->amax.end(), SAMP_E_CALIBRATION, "calibration table is missing site '" + site + "'");
+  return it->second;
+}
+static double sc(samp_engine* e, const std::string& site) { return site_scale(need_amax(e, site)); }
+static std::string lsite(int i, const char* blk, const char* name) {
+  return "L" + std::to_string(i) + "." + blk + "." + name;
+}
+static std::string input_site(int i) { return i == 0 ? "embed.out" : lsite(i, "attn", "in"); }
+
+// required sites for a plan, as PrecisionPlan.required_sites (encoder.py:126-136) + MHA-only
+static std::set<std::string> required_sites(const uint8_t* prec, int L) {
+  std::set<std::string> s;
+  for (int i = 0; i < L; ++i) {
+    if (prec[i] == SAMP_LAYER_FULL_INT8 || prec[i] == SAMP_LAYER_MHA_INT8) {
+      s.insert(input_site(i));
+      for (const char* n : {"q", "k", "v", "softmax", "out_in"}) s.insert(lsite(i, "attn", n));
+      s.insert(lsite(i, "ffn", "in"));
+      if (prec[i] == SAMP_LAYER_FULL_INT8) s.insert(lsite(i, "ffn", "mid"));
+    } else if (prec[i] == SAMP_LAYER_FFN_INT8) {
+      s.insert(lsite(i, "ffn", "in"));
+      s.insert(lsite(i, "ffn", "mid"));
+    }
+  }
+  return s;
+}
+
+static void record(samp_engine* e, const std::string& name, int layer, const void* dev, size_t bytes) {
+  if (!e->capture) return;
+  std::vector<uint8_t> host(bytes);
+  SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));
+  SAMP_CUDA(cudaMemcpy(host.data(), dev, bytes, cudaMemcpyDeviceToHost));
+  e->stages[name + "@" + std::to_string(layer)] = std::move(host);
+}
+
+static cudaEvent_t take_event(samp_engine* e) {
+  if (e->event_pool.empty()) {
+    cudaEvent_t ev;
+    SAMP_CUDA(cudaEventCreate(&ev));
+    return ev;
+  }
+  cudaEvent_t ev = e->event_pool.back();
+  e->event_pool.pop_back();
+  return ev;
+}
+
+// launch through `fn` (returns cudaError_t); with profiling on, bracket it with CUDA
+// events on the engine stream (the stream every kernel is launched on)
+template <class F>
+static void run_kernel(samp_engine* e, const char* what, F&& fn) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (e->profiling) {
+    a = take_event(e);
+    b = take_event(e);
+    SAMP_CUDA(cudaEventRecord(a, e->stream_in_use));
+  }
+  cudaError_t err = fn();
+  if (err == cudaSuccess) err = cudaGetLastError();
+  SAMP_REQUIRE(err == cudaSuccess, SAMP_E_DEVICE, std::string(what) + ": " + cudaGetErrorString(err));
+  if (e->profiling) {
+    SAMP_CUDA(cudaEventRecord(b, e->stream_in_use));
+    e->pending.push_back({what, a, b});
+  }
+  e->launches++;
+}
+#define check_launch(E, CALL, NAME) run_kernel((E), (NAME), [&]() { return (CALL); })
+
+static void launch_attention(samp_engine* e, bool f16, const AttnParams& p) {
+  const Geometry& g = e->geo;
+  check_launch(e, f16 ? launch_attention_f16(e->act.att_qkv_f16, p, g.ntiles, e->d.num_heads, g.max_nkp, e->stream_in_use)
+                      : launch_attention_i8(e->act.att_qkv_i8, p, g.ntiles, e->d.num_heads, g.max_nkp, e->stream_in_use),
+               f16 ? "attention_f16" : "attention_i8");
+}
+
+static int tmem_cols_for_keys(int nkp) {
+  int c = 64;
+  while (c < nkp) c *= 2;
+  return c;
+}
+
+// one encoder layer; `in_q` = index of xq holding this layer's input codes (INT8 inputs)
+static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
+  const int L = e->d.num_layers, H = e->d.hidden, I = e->d.intermediate, T = e->geo.T;
+  const uint8_t p = prec[i];
+  const bool next_int8 = i + 1 < L && (prec[i + 1] == SAMP_LAYER_FULL_INT8 || prec[i + 1] == SAMP_LAYER_MHA_INT8);
+  Activations& a = e->act;
+  LayerDev& w = e->layers[i];
+  const Tiles& t = e->tiles;
+  const float eps = f32(e->d.layernorm_eps);
+  const int fp16_store = e->d.fp16_storage;
+  const bool int8_attn = p == SAMP_LAYER_FULL_INT8 || p == SAMP_LAYER_MHA_INT8;
+  cudaStream_t st = e->stream_in_use;
+
+  // ---------------- attention block
+  double s_in = 0;
+  if (int8_attn) {
+    s_in = sc(e, input_site(i));
+    record(e, "in_q", i, a.xq[cur], size_t(T) * H);
+    EpiQKV::Params qp{};
+    qp.out = a.qkv_i8;
+    qp.ldo = 3 * H;
+    qp.bias = w.qkv_b;
+    qp.block_cols = H;
+    qp.mult0 = mult_of(s_in, w.s_w[0]);
+    qp.mult1 = mult_of(s_in, w.s_w[1]);
+    qp.mult2 = mult_of(s_in, w.s_w[2]);
+    qp.sout0 = f32(sc(e, lsite(i, "attn", "q")));
+    qp.sout1 = f32(sc(e, lsite(i, "attn", "k")));
+    qp.sout2 = f32(sc(e, lsite(i, "attn", "v")));
+    check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
+    record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
+    AttnParams ap{};
+    ap.ctx_out = a.ctx_i8;
+    ap.tile_seq = e->geo.d_tile_seq;
+    ap.tile_q0 = e->geo.d_tile_q0;
+    ap.seq_start = e->geo.d_seq_start;
+    ap.att_len = e->geo.d_att_len;
+    ap.hidden = H;
+    const double sq = sc(e, lsite(i, "attn", "q")), sk = sc(e, lsite(i, "attn", "k"));
+    const double sv = sc(e, lsite(i, "attn", "v")), ssm = sc(e, lsite(i, "attn", "softmax"));
+    ap.mult_scores = f32(sq * sk / std::sqrt(double(H / e->d.num_heads)));
+    ap.s_softmax = f32(ssm);
+    ap.mult_ctx = mult_of(ssm, sv);
+    ap.s_ctx = f32(sc(e, lsite(i, "attn", "out_in")));
+    ap.tmem_cols = tmem_cols_for_keys(e->geo.max_nkp);
+    launch_attention(e, false, ap);
+    record(e, "ctx_q", i, a.ctx_i8, size_t(T) * H);
+    EpiResLN::Params lp{};
+    lp.bias = w.ob;
+    lp.res_i8 = a.xq[cur];
+    lp.res_scale = f32(s_in);
+    lp.gamma = w.ln1_g;
+    lp.beta = w.ln1_b;
+    lp.mult = mult_of(sc(e, lsite(i, "attn", "out_in")), w.s_w[3]);
+    lp.eps = eps;
+    lp.hidden = H;
+    lp.out_i8 = a.ffn_in_i8;
+    lp.s_out = f32(sc(e, lsite(i, "ffn", "in")));
+    if (p == SAMP_LAYER_MHA_INT8) {  // FP FFN consumes dequant(ffn.in codes)
+      lp.deq_outputs = 1;
+      lp.out_f32 = a.ln1_f32;
+      lp.out_f16 = a.ln1_f16;
+    }
+    check_launch(e, gemm_ln_i8(t, a.a_ctx_i8, w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
+    record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
+  } else {
+    record(e, "in_f32", i, a.hid_f32, size_t(T) * H * 4);
+    EpiF16Out::Params qp{a.qkv_f16, 3 * H, w.qkv_b, 0};
+    check_launch(e, gemm_f16out(t.bn_qkv, a.a_hid_f16, w.m_qkv_f16, T, 3 * H, 2 * H, qp, st), "qkv_f16");
+    AttnParams ap{};
+    ap.ctx_out = a.ctx_f16;
+    ap.tile_seq = e->geo.d_tile_seq;
+    ap.tile_q0 = e->geo.d_tile_q0;
+    ap.seq_start = e->geo.d_seq_start;
+    ap.att_len = e->geo.d_att_len;
+    ap.hidden = H;
+    ap.mult_scores = f32(1.0 / std::sqrt(double(H / e->d.num_heads)));
+    ap.tmem_cols = tmem_cols_for_keys(e->geo.max_nkp);
+    launch_attention(e, true, ap);
+    EpiResLN::Params lp{};
+    lp.bias = w.ob;
+    lp.res_f32 = a.hid_f32;
+    lp.gamma = w.ln1_g;
+    lp.beta = w.ln1_b;
+    lp.acc_is_f32 = 1;
+    lp.eps = eps;
+    lp.hidden = H;
+    if (p == SAMP_LAYER_FFN_INT8) {
+      lp.out_i8 = a.ffn_in_i8;
+      lp.s_out = f32(sc(e, lsite(i, "ffn", "in")));
+    } else {
+      lp.out_f32 = a.ln1_f32;
+      lp.out_f16 = a.ln1_f16;
+      lp.f16_round = fp16_store;
+    }
+    check_launch(e, gemm_ln_f16(t, a.a_ctx_f16, w.m_wo_f16, T, H, 2 * H, lp, st), "outproj_f16");
+    if (p == SAMP_LAYER_FFN_INT8) record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
+    else record(e, "ln1_f32", i, a.ln1_f32, size_t(T) * H * 4);
+  }
+
+  // ---------------- feed-forward block; output goes to xq[cur^1] (codes) or hid_f32/f16
+  EpiResLN::Params lp{};
+  lp.gamma = w.ln2_g;
+  lp.beta = w.ln2_b;
+  lp.eps = eps;
+  lp.hidden = H;
+  lp.bias = w.b2;
+  if (next_int8) {
+    lp.out_i8 = a.xq[cur ^ 1];
+    lp.s_out = f32(sc(e, input_site(i + 1)));
+  } else {
+    lp.out_f32 = a.hid_f32;
+    lp.out_f16 = a.hid_f16;
+  }
+  if (p == SAMP_LAYER_FULL_INT8 || p == SAMP_LAYER_FFN_INT8) {
+    const double s_fin = sc(e, lsite(i, "ffn", "in")), s_mid = sc(e, lsite(i, "ffn", "mid"));
+    EpiGeluQuant::Params gp{a.mid_i8, I, w.b1, mult_of(s_fin, w.s_w[4]), f32(s_mid)};
+    check_launch(e, gemm_gelu_i8(t.bn_ffn1, a.a_ffn_in, w.m_w1_i8, T, I, H, gp, st), "ffn1_i8");
+    record(e, "mid_q", i, a.mid_i8, size_t(T) * I);
+    lp.res_i8 = a.ffn_in_i8;
+    lp.res_scale = f32(s_fin);
+    lp.mult = mult_of(s_mid, w.s_w[5]);
+    check_launch(e, gemm_ln_i8(t, a.a_mid_i8, w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
+  } else {
+    EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1};
+    check_launch(e, gemm_f16out(t.bn_ffn1, a.a_ln1_f16, w.m_w1_f16, T, I, 2 * H, gp, st), "ffn1_f16");
+    lp.res_f32 = a.ln1_f32;
+    lp.acc_is_f32 = 1;
+    lp.f16_round = (p == SAMP_LAYER_FP) ? fp16_store : 0;
+    check_launch(e, gemm_ln_f16(t, a.a_mid_f16, w.m_w2_f16, T, H, 2 * I, lp, st), "ffn2_f16");
+  }
+  if (next_int8) {
+    cur ^= 1;
+    record(e, "out_q", i, a.xq[cur], size_t(T) * H);
+  } else {
+    record(e, "out_f32", i, a.hid_f32, size_t(T) * H * 4);
+  }
+}
+
+}  // namespace samp
+
+using namespace samp;
+
+extern "C" int samp_engine_create(const samp_model_desc* desc, int device, samp_engine** out) {
+  return guarded([&] {
+    SAMP_REQUIRE(desc && out, SAMP_E_CONFIGURATION, "null argument");
+    const samp_model_desc& d = *desc;
+    SAMP_REQUIRE(d.num_layers >= 1 && d.hidden >= 1 && d.num_heads >= 1 && d.intermediate >= 1 &&
+                     d.vocab_size >= 1 && d.max_position >= 1 && d.type_vocab_size >= 1 && d.num_labels >= 1,
+                 SAMP_E_CONFIGURATION, "model sizes must be >= 1");
+    SAMP_REQUIRE(d.hidden % d.num_heads == 0, SAMP_E_CONFIGURATION, "hidden not divisible by num_heads");
+    SAMP_REQUIRE(d.hidden / d.num_heads == 64, SAMP_E_CONFIGURATION,
+                 "the B200 kernels are built for head_dim = 64 (BERT-base/large); got " +
+                     std::to_string(d.hidden / d.num_heads));
+    SAMP_REQUIRE(d.max_position <= ATT_MAX_KEYS, SAMP_E_CONFIGURATION, "max_position > 512 is not supported");
+    SAMP_REQUIRE(d.num_labels <= HEAD_MAX_LABELS, SAMP_E_CONFIGURATION, "num_labels > 64 is not supported");
+    Tiles t = choose_tiles(d.hidden, d.intermediate);
+    SAMP_REQUIRE(t.bn_qkv && t.bn_ffn1 && t.bn_ln, SAMP_E_CONFIGURATION,
+                 "unsupported hidden/intermediate sizes for the tcgen05 tiles (need multiples of 64, hidden in "
+                 "{64,128,256,384,512,768,1024})");
+    int rc = samp_device_check(device);
+    if (rc != SAMP_OK) throw SampError(rc, samp_last_error());
+    SAMP_CUDA(cudaSetDevice(device));
+    auto* e = new samp_engine();
+    e->d = d;
+    e->device = device;
+    e->tiles = t;
+    e->layers.resize(d.num_layers);
+    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete e;
+      throw SampError(SAMP_E_DEVICE, "cudaStreamCreate failed");
+    }
+    e->stream_in_use = e->stream;
+    *out = e;
+  });
+}
+
+extern "C" void samp_engine_destroy(samp_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
+  cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+extern "C" int samp_load_embeddings(samp_engine* e, const float* word, const float* position,
+                                    const float* token_type, const float* g, const float* b) {
+  return guarded([&] {
+    SAMP_CUDA(cudaSetDevice(e->device));
+    const size_t H = e->d.hidden;
+    auto up = [&](const float* src, size_t n) {
+      float* dst = e->mem.alloc<float>(n);
+      SAMP_CUDA(cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice));
+      return dst;
+    };
+    e->word = up(word, size_t(e->d.vocab_size) * H);
+    e->position = up(position, size_t(e->d.max_position) * H);
+    e->token_type = up(token_type, size_t(e->d.type_vocab_size) * H);
+    e->emb_g = up(g, H);
+    e->emb_b = up(b, H);
+    e->emb_loaded = true;
+  });
+}
+
+extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t) {
+  return guarded([&] {
+    SAMP_REQUIRE(layer >= 0 && layer < e->d.num_layers, SAMP_E_CONFIGURATION, "layer index out of range");
+    SAMP_CUDA(cudaSetDevice(e->device));
+    const int H = e->d.hidden, I = e->d.intermediate;
+    LayerDev& w = e->layers[layer];
+    // per-tensor INT8 weight scales exactly as quantize_weight (encoder.py:191-194)
+    const float* mats[6] = {t[0], t[2], t[4], t[6], t[10], t[12]};
+    const size_t sizes[6] = {size_t(H) * H, size_t(H) * H, size_t(H) * H, size_t(H) * H, size_t(H) * I, size_t(I) * H};
+    for (int k = 0; k < 6; ++k) w.s_w[k] = site_scale(host_amax(mats[k], sizes[k]));
+    w.qkv_i8 = e->mem.alloc<int8_t>(size_t(3) * H * H);
+    w.wo_i8 = e->mem.alloc<int8_t>(size_t(H) * H);
+    w.w1_i8 = e->mem.alloc<int8_t>(size_t(I) * H);
+    w.w2_i8 = e->mem.alloc<int8_t>(size_t(H) * I);
+    w.qkv_f16 = e->mem.alloc<__half>(size_t(3) * H * H);
+    w.wo_f16 = e->mem.alloc<__half>(size_t(H) * H);
+    w.w1_f16 = e->mem.alloc<__half>(size_t(I) * H);
+    w.w2_f16 = e->mem.alloc<__half>(size_t(H) * I);
+    float* tmp = e->mem.alloc<float>(size_t(H) * std::max(H, I));
+    auto pack = [&](const float* src, int K, int N, double scale, int8_t* oi8, __half* of16, int row_off) {
+      SAMP_CUDA(cudaMemcpy(tmp, src, size_t(K) * N * 4, cudaMemcpyHostToDevice));
+      SAMP_CUDA(launch_pack_weight(tmp, K, N, f32(scale), oi8, of16, row_off, 0));
+      SAMP_CUDA(cudaDeviceSynchronize());
+    };
+    pack(t[0], H, H, w.s_w[0], w.qkv_i8, w.qkv_f16, 0);
+    pack(t[2], H, H, w.s_w[1], w.qkv_i8, w.qkv_f16, H);
+    pack(t[4], H, H, w.s_w[2], w.qkv_i8, w.qkv_f16, 2 * H);
+    pack(t[6], H, H, w.s_w[3], w.wo_i8, w.wo_f16, 0);
+    pack(t[10], H, I, w.s_w[4], w.w1_i8, w.w1_f16, 0);
+    pack(t[12], I, H, w.s_w[5], w.w2_i8, w.w2_f16, 0);
+    e->mem.release(tmp);
+    auto up = [&](const float* src, size_t n) {
+      float* dst = e->mem.alloc<float>(n);
+      SAMP_CUDA(cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice));
+      return dst;
+    };
+    w.qkv_b = e->mem.alloc<float>(size_t(3) * H);
+    SAMP_CUDA(cudaMemcpy(w.qkv_b, t[1], H * 4, cudaMemcpyHostToDevice));
+    SAMP_CUDA(cudaMemcpy(w.qkv_b + H, t[3], H * 4, cudaMemcpyHostToDevice));
+    SAMP_CUDA(cudaMemcpy(w.qkv_b + 2 * H, t[5], H * 4, cudaMemcpyHostToDevice));
+    w.ob = up(t[7], H);
+    w.ln1_g = up(t[8], H);
+    w.ln1_b = up(t[9], H);
+    w.b1 = up(t[11], I);
+    w.b2 = up(t[13], H);
+    w.ln2_g = up(t[14], H);
+    w.ln2_b = up(t[15], H);
+    const Tiles& tl = e->tiles;
+    w.m_qkv_i8 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, tl.bn_qkv);
+    w.m_wo_i8 = tmap_i8(w.wo_i8, H, H, H, 128, tl.bn_ln);
+    w.m_w1_i8 = tmap_i8(w.w1_i8, I, H, H, 128, tl.bn_ffn1);
+    w.m_w2_i8 = tmap_i8(w.w2_i8, H, I, I, 128, tl.bn_ln);
+    w.m_qkv_f16 = tmap_f16(w.qkv_f16, 3 * H, H, H, 64, tl.bn_qkv);
+    w.m_wo_f16 = tmap_f16(w.wo_f16, H, H, H, 64, tl.bn_ln);
+    w.m_w1_f16 = tmap_f16(w.w1_f16, I, H, H, 64, tl.bn_ffn1);
+    w.m_w2_f16 = tmap_f16(w.w2_f16, H, I, I, 64, tl.bn_ln);
+    w.loaded = true;
+  });
+}
+
+extern "C" int samp_load_heads(samp_engine* e, const float* pool_w, const float* pool_b, const float* head_w,
+                               const float* head_b) {
+  return guarded([&] {
+    SAMP_CUDA(cudaSetDevice(e->device));
+    const int H = e->d.hidden, L = e->d.num_labels;
+    auto up_t = [&](const float* src, int K, int N) {  // (in,out) -> (out,in)
+      float* raw = e->mem.alloc<float>(size_t(K) * N);
+      float* dst = e->mem.alloc<float>(size_t(K) * N);
+      SAMP_CUDA(cudaMemcpy(raw, src, size_t(K) * N * 4, cudaMemcpyHostToDevice));
+      SAMP_CUDA(launch_transpose_f32(raw, K, N, dst, 0));
+      SAMP_CUDA(cudaDeviceSynchronize());
+      e->mem.release(raw);
+      return dst;
+    };
+    if (pool_w) {
+      e->pool_w = e->mem.alloc<float>(size_t(H) * H);
+      SAMP_CUDA(cudaMemcpy(e->pool_w, pool_w, size_t(H) * H * 4, cudaMemcpyHostToDevice));
+      e->pool_b = e->mem.alloc<float>(H);
+      SAMP_CUDA(cudaMemcpy(e->pool_b, pool_b, H * 4, cudaMemcpyHostToDevice));
+    }
+    e->head_wt = up_t(head_w, H, L);
+    e->head_b = e->mem.alloc<float>(L);
+    SAMP_CUDA(cudaMemcpy(e->head_b, head_b, L * 4, cudaMemcpyHostToDevice));
+    e->heads_loaded = true;
+  });
+}
+
+extern "C" int samp_weight_scales(samp_engine* e, int layer, double* out6) {
+  return guarded([&] {
+    SAMP_REQUIRE(layer >= 0 && layer < e->d.num_layers && e->layers[layer].loaded, SAMP_E_CONFIGURATION,
+                 "layer not loaded");
+    for (int k = 0; k < 6; ++k) out6[k] = e->layers[layer].s_w[k];
+  });
+}
+
+extern "C" int samp_set_site_amax(samp_engine* e, const char* site, double amax) {
+  return guarded([&] { e->amax[site] = amax; });
+}
+
+extern "C" int samp_clear_calibration(samp_engine* e) {
+  return guarded([&] { e->amax.clear(); });
+}
+
+extern "C" int samp_set_capture(samp_engine* e, int on) {
+  return guarded([&] {
+    e->capture = on != 0;
+    if (e->capture) e->stages.clear();  // turning capture off keeps the last forward's stages
+  });
+}
+
+extern "C" int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, size_t capacity,
+                                size_t* bytes) {
+  return guarded([&] {
+    auto it = e->stages.find(std::string(name) + "@" + std::to_string(layer));
+    SAMP_REQUIRE(it != e->stages.end(), SAMP_E_CONFIGURATION,
+                 std::string("no captured stage ") + name + " for layer " + std::to_string(layer));
+    if (bytes) *bytes = it->second.size();
+    if (dst) {
+      SAMP_REQUIRE(capacity >= it->second.size(), SAMP_E_DIMENSION, "destination too small");
+      std::memcpy(dst, it->second.data(), it->second.size());
+    }
+  });
+}
+
+extern "C" int samp_sync(samp_engine* e) {
+  return guarded([&] { SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use)); });
+}
+
+extern "C" int samp_last_launch_count(samp_engine* e) { return e ? e->launches : 0; }
+
+extern "C" int samp_set_profiling(samp_engine* e, int on) {
+  return guarded([&] {
+    e->profiling = on != 0;
+    e->prof.clear();
+  });
+}
+
+// sync, fold pending event pairs into per-kernel totals, and write them as JSON
+// {"name": [total_ms, launches], ...} into buf
+extern "C" int samp_profile_report(samp_engine* e, char* buf, size_t cap) {
+  return guarded([&] {
+    SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));
+    for (auto& p : e->pending) {
+      float ms = 0;
+      SAMP_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+      auto& slot = e->prof[p.name];
+      slot.first += ms;
+      slot.second += 1;
+      e->event_pool.push_back(p.a);
+      e->event_pool.push_back(p.b);
+    }
+    e->pending.clear();
+    std::string js = "{";
+    bool first = true;
+    for (auto& kv : e->prof) {
+      js += (first ? "\"" : ", \"") + kv.first + "\": [" + std::to_string(kv.second.first) + ", " +
+            std::to_string(kv.second.second) + "]";
+      first = false;
+    }
+    js += "}";
+    SAMP_REQUIRE(buf && cap > js.size(), SAMP_E_DIMENSION, "profile buffer too small");
+    std::memcpy(buf, js.c_str(), js.size() + 1);
+  });
+}
+
+extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, const int32_t* seq_start,
+                            const int32_t* att_len, const int32_t* ids, const int32_t* segs, int32_t io,
+                            const samp_outputs* out, void* stream_arg) {
+  return guarded([&] {
+    const samp_model_desc& d = e->d;
+    const int L = d.num_layers, H = d.hidden;
+    // ---------------- validation (before any device work, like the reference)
+    SAMP_REQUIRE(e->emb_loaded, SAMP_E_CONFIGURATION, "embeddings not loaded");
+    for (int i = 0; i < L; ++i) {
+      SAMP_REQUIRE(prec[i] <= SAMP_LAYER_MHA_INT8, SAMP_E_CONFIGURATION, "bad layer precision code");
+      SAMP_REQUIRE(e->layers[i].loaded, SAMP_E_CONFIGURATION, "layer " + std::to_string(i) + " not loaded");
+    }
+    {
+      std::vector<std::string> missing;
+      for (const auto& s : required_sites(prec, L))
+        if (!e->amax.count(s)) missing.push_back(s);
+      if (!missing.empty()) {
+        std::string msg = "calibration table is missing sites: ";
+        for (size_t k = 0; k < missing.size(); ++k) msg += (k ? ", " : "") + missing[k];
+        throw SampError(SAMP_E_CALIBRATION, msg);
+      }
+    }
+    SAMP_REQUIRE(nseq >= 1, SAMP_E_INPUT, "empty batch");
+    SAMP_REQUIRE(seq_start[0] == 0, SAMP_E_INPUT, "seq_start[0] must be 0");
+    for (int s = 0; s < nseq; ++s) {
+      const int S = seq_start[s + 1] - seq_start[s];
+      SAMP_REQUIRE(S >= 1, SAMP_E_INPUT, "empty token id sequence");
+      SAMP_REQUIRE(S <= d.max_position, SAMP_E_INPUT,
+                   "sequence length " + std::to_string(S) + " exceeds max_position " + std::to_string(d.max_position));
+    }
+    const int T = seq_start[nseq];
+    if (io == SAMP_IO_HOST) {
+      for (int k = 0; k < T; ++k) {
+        SAMP_REQUIRE(ids[k] >= 0 && ids[k] < d.vocab_size, SAMP_E_INPUT,
+                     "token id out of range [0, " + std::to_string(d.vocab_size) + ")");
+        SAMP_REQUIRE(segs[k] >= 0 && segs[k] < d.type_vocab_size, SAMP_E_INPUT,
+                     "segment id out of range [0, " + std::to_string(d.type_vocab_size) + ")");
+      }
+    }
+    const int head = out ? out->head : SAMP_HEAD_NONE;
+    if (head != SAMP_HEAD_NONE)
+      SAMP_REQUIRE(e->heads_loaded && (head != SAMP_HEAD_CLASSIFY || e->pool_w), SAMP_E_CONFIGURATION,
+                   "head weights not loaded");
+    SAMP_CUDA(cudaSetDevice(e->device));
+    // launch on the caller's stream when given (so its events / graphs see every kernel)
+    e->stream_in_use = stream_arg ? static_cast<cudaStream_t>(stream_arg) : e->stream;
+    set_geometry(e, nseq, seq_start, att_len);
+    e->launches = 0;
+    e->stages.clear();
+    Activations& a = e->act;
+    cudaStream_t st = e->stream_in_use;
+    // ---------------- inputs
+    if (io == SAMP_IO_HOST) {
+      if (e->pinned_cap < 2 * T) {
+        if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
+        e->pinned_cap = std::max(2 * T, 8192);
+        SAMP_CUDA(cudaMallocHost(&e->pinned_ids, size_t(e->pinned_cap) * sizeof(int)));
+      }
+      SAMP_CUDA(cudaStreamSynchronize(st));  // staging buffer reuse
+      std::memcpy(e->pinned_ids, ids, size_t(T) * 4);
+      std::memcpy(e->pinned_ids + T, segs, size_t(T) * 4);
+      SAMP_CUDA(cudaMemcpyAsync(a.ids, e->pinned_ids, size_t(T) * 4, cudaMemcpyHostToDevice, st));
+      SAMP_CUDA(cudaMemcpyAsync(a.segs, e->pinned_ids + T, size_t(T) * 4, cudaMemcpyHostToDevice, st));
+    } else {
+      SAMP_CUDA(cudaMemcpyAsync(a.ids, ids, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+      SAMP_CUDA(cudaMemcpyAsync(a.segs, segs, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    // ---------------- embedding (+ quantize at embed.out when layer 0 is INT8-attention)
+    const bool first_int8 = prec[0] == SAMP_LAYER_FULL_INT8 || prec[0] == SAMP_LAYER_MHA_INT8;
+    EmbedParams ep{};
+    ep.ids = a.ids;
+    ep.segs = a.segs;
+    ep.pos = a.pos;
+    ep.word = e->word;
+    ep.position = e->position;
+    ep.token_type = e->token_type;
+    ep.gamma = e->emb_g;
+    ep.beta = e->emb_b;
+    ep.eps = f32(d.layernorm_eps);
+    ep.hidden = H;
+    ep.T = T;
+    ep.f16_round = d.fp16_storage;
+    ep.out_f32 = a.hid_f32;
+    ep.out_f16 = a.hid_f16;
+    if (first_int8) {
+      ep.out_i8 = a.xq[0];
+      ep.s_out = f32(sc(e, "embed.out"));
+    }
+    check_launch(e, launch_embed(ep, st), "embed");
+    record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
+    int cur = 0;
+    for (int i = 0; i < L; ++i) run_layer(e, i, prec, cur);
+    // ---------------- heads + outputs (final hidden is always F32 in hid_f32)
+    const int nl = d.num_labels;
+    if (head != SAMP_HEAD_NONE) {
+      HeadParams hp{};
+      hp.hidden = a.hid_f32;
+      hp.seq_start = e->geo.d_seq_start;
+      hp.pool_w = e->pool_w;
+      hp.pooled = a.pooled;
+      hp.pool_b = e->pool_b;
+      hp.head_wt = e->head_wt;
+      hp.head_b = e->head_b;
+      hp.hidden_size = H;
+      hp.num_labels = nl;
+      hp.nseq = nseq;
+      hp.T = T;
+      hp.logits = a.logits;
+      hp.probs = a.probs;
+      hp.labels = a.labels;
+      check_launch(e, head == SAMP_HEAD_CLASSIFY ? launch_classify(hp, st) : launch_tag(hp, st), "head");
+    }
+    const cudaMemcpyKind kind = io == SAMP_IO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (out) {
+      if (out->hidden) SAMP_CUDA(cudaMemcpyAsync(out->hidden, a.hid_f32, size_t(T) * H * 4, kind, st));
+      const size_t rows = head == SAMP_HEAD_CLASSIFY ? nseq : T;
+      if (head != SAMP_HEAD_NONE) {
+        if (out->logits) SAMP_CUDA(cudaMemcpyAsync(out->logits, a.logits, rows * nl * 4, kind, st));
+        if (out->probs) SAMP_CUDA(cudaMemcpyAsync(out->probs, a.probs, rows * nl * 4, kind, st));
+        if (out->labels) SAMP_CUDA(cudaMemcpyAsync(out->labels, a.labels, rows * 4, kind, st));
+      }
+    }
+    if (io == SAMP_IO_HOST) SAMP_CUDA(cudaStreamSynchronize(st));
+  });
+}

@@ -4,15 +4,20 @@
 //                                 W: weights stored transposed Wt[N][K] (K-major)
 //
 // One CTA computes a 128 x BN tile (UMMA M=128, N=BN, cta_group::1); int32 (kind::i8)
-// or f32 (kind::f16) accumulators live in TMEM.  Warp roles (192 threads):
+// or f32 (kind::f16) accumulators live in TMEM.  Warp roles (64 + 32*NE threads):
 //   warp 0     TMA producer: 128B-swizzled A/B k-blocks (128 bytes of K) into a
 //              STAGES-deep smem ring, completion on full[] mbarriers
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs of 32 B of K
 //              per k-block); tcgen05.commit frees ring slots and finally signals tmem_full
-//   warps 2-5  epilogue: thread t owns accumulator row t (TMEM lane t) and streams its
-//              row out of TMEM with tcgen05.ld.32x32b — a whole output row per thread is
+//   warps 2..  NE epilogue warps.  TMEM lane quarter q may only be read by warps with
+//              warp%4 == q, so thread (warp, lane) owns accumulator row 32*(warp%4)+lane and
+//              the column half (warp-2)/4 when NE == 8.  Owning a (half) row per thread is
 //              what lets the fused LayerNorm epilogue reproduce numpy's pairwise tree
-//              sequentially, bit-for-bit (numerics.cuh).
+//              sequentially, bit-for-bit (numerics.cuh): NE == 8 is only used when the two
+//              column halves are exact subtrees of that tree.
+// The epilogues dominate (bit-exact GELU / quantize / LayerNorm cost far more than the
+// MMAs at BERT shapes), so the ring is kept small enough (<= ~100 KB) for two CTAs per SM:
+// one CTA's epilogue overlaps the other's TMA + MMA main loop.
 // Row-complete epilogues (LayerNorm over N = hidden) run as a cluster of CLUSTER CTAs
 // along N; each CTA reduces its BN columns (an exact numpy subtree) and partial sums
 // are exchanged through DSMEM.
@@ -27,7 +32,6 @@
 namespace samp {
 
 constexpr int GEMM_BM = 128;
-constexpr int GEMM_THREADS = 192;
 constexpr int GEMM_EPI_WARP0 = 2;
 
 __host__ __device__ constexpr int tmem_cols_for(int n) {
@@ -46,42 +50,39 @@ struct GemmLayout {
   static constexpr int TOTAL = EPI_OFF_ALIGNED + EPI_SMEM + 1024;     // + alignment slack
 };
 
-// Shared epilogue context: where this thread's accumulator row lives.
+// Shared epilogue context: where this thread's accumulator (half) row lives.
 struct EpiCtx {
-  uint32_t taddr;    // TMEM address of (this thread's lane, column 0)
+  uint32_t taddr;    // TMEM address of (this thread's lane, column c0)
   int row;           // global output row
-  int ep_tid;        // 0..127 (== tile row)
+  int tile_row;      // 0..127
   int n0;            // first output column of the tile
+  int c0;            // first tile column this thread owns
+  int ncols;         // columns this thread owns (BN or BN/2)
+  int half;          // 0/1 (NE == 8) or 0
   int M;             // valid rows
+  int ep_tid;        // 0 .. 32*NE-1
+  int ne_threads;    // 32*NE
 };
 
-// Sum partials of the CLUSTER CTAs in numpy's tree order (each CTA holds one subtree).
-template <int CLUSTER>
-__device__ __forceinline__ float cluster_tree_sum(float* red, int ep_tid, float mine) {
-  if constexpr (CLUSTER == 1) {
-    return mine;
-  } else {
-    red[ep_tid] = mine;
-    cluster_sync_all();
-    float p[CLUSTER];
-#pragma unroll
-    for (int r = 0; r < CLUSTER; ++r) p[r] = dsmem_ld_f32(&red[ep_tid], r);
-    if constexpr (CLUSTER == 2) return __fadd_rn(p[0], p[1]);
-    else return __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
-  }
+// named barrier among the epilogue warps only
+__device__ __forceinline__ void epi_bar_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" :: "r"(nthreads) : "memory");
 }
 
-template <int KIND, int BN, int STAGES, int CLUSTER, class Epi>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
+__global__ void __launch_bounds__(64 + 32 * NE, 2)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             int M, int k_bytes, const typename Epi::Params ep) {
   using Lay = GemmLayout<BN, STAGES, Epi::SMEM_BYTES>;
   constexpr int TMEM_COLS = tmem_cols_for(BN);
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+  static_assert(NE == 4 || (NE == 8 && (BN / 2) % 32 == 0), "epilogue split");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ array keeps the shared address space visible
+  // to the compiler (LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
@@ -106,7 +107,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     tma_prefetch(&map_b);
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
-  if (warp >= GEMM_EPI_WARP0) Epi::prologue(ep, epi_smem, threadIdx.x - GEMM_EPI_WARP0 * 32);
+  if (warp >= GEMM_EPI_WARP0) Epi::prologue(ep, epi_smem, threadIdx.x - GEMM_EPI_WARP0 * 32, 32 * NE);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,12 +147,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   } else {
     const int ep_tid = threadIdx.x - GEMM_EPI_WARP0 * 32;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = NE == 8 ? int(warp - GEMM_EPI_WARP0) / 4 : 0;
     const int tile_row = quarter * 32 + lane_id();
+    const int c0 = half * (BN / (NE / 4));
     mbar_wait(tmem_full, 0);
     tc_fence_after();
-    EpiCtx c{tmem + (uint32_t(quarter * 32) << 16), m0 + tile_row, tile_row, n0, M};
-    (void)ep_tid;
-    Epi::template run<BN, CLUSTER>(ep, c, epi_smem);
+    EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(c0), m0 + tile_row, tile_row, n0, c0,
+             BN / (NE / 4), half, M, ep_tid, 32 * NE};
+    Epi::template run<BN, CLUSTER, NE>(ep, c, epi_smem);
   }
   // non-epilogue warps mirror the epilogue's cluster barriers
   if (warp < GEMM_EPI_WARP0) {
@@ -166,6 +169,27 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   }
 }
 
+__device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
+  return (uint32_t(a) & 0xffu) | ((uint32_t(b) & 0xffu) << 8) | ((uint32_t(c) & 0xffu) << 16) |
+         (uint32_t(d) << 24);
+}
+
+__device__ __forceinline__ void store32_i8(int8_t* dst, const int (&q)[32]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = pack4_i8(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+  reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+__device__ __forceinline__ void load_bias32(const float* b, float (&out)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(b) + j);
+    out[4 * j] = v.x; out[4 * j + 1] = v.y; out[4 * j + 2] = v.z; out[4 * j + 3] = v.w;
+  }
+}
+
 // ------------------------------------------------------------------ epilogues
 
 // raw int32 / f32 accumulator store (kernel tests, parity of the accumulators)
@@ -176,27 +200,22 @@ struct EpiStoreAcc {
   };
   static constexpr int SMEM_BYTES = 0;
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t*, int) {}
-  template <int BN, int CLUSTER>
+  __device__ static void prologue(const Params&, uint8_t*, int, int) {}
+  template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t*) {
 #pragma unroll 1
-    for (int col = 0; col < BN; col += 32) {
+    for (int col = 0; col < c.ncols; col += 32) {
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
       tmem_wait_ld();
       if (c.row < c.M) {
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint32_t*>(p.out) + size_t(c.row) * p.ldc + c.n0 + col);
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint32_t*>(p.out) + size_t(c.row) * p.ldc + c.n0 + c.c0 + col);
 #pragma unroll
         for (int j = 0; j < 8; ++j) dst[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
       }
     }
   }
 };
-
-__device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
-  return (uint32_t(a) & 0xffu) | ((uint32_t(b) & 0xffu) << 8) | ((uint32_t(c) & 0xffu) << 16) |
-         ((uint32_t(d) & 0xffu) << 24);
-}
 
 // Fused QKV: per column block (q|k|v) dequant F32(acc)*F32(s_in*s_w) + bias, quantize
 // at the block's site (reference encoder.py:355-366).
@@ -206,37 +225,31 @@ struct EpiQKV {
     int ldo;
     const float* bias;    // [3H]
     int block_cols;       // H
-    float mult[3];        // F32(double(s_in) * double(s_w{q,k,v}))
-    float s_out[3];       // F32(scale(L.attn.{q,k,v}))
+    float mult0, mult1, mult2;     // F32(double(s_in) * double(s_w{q,k,v}))
+    float sout0, sout1, sout2;     // F32(scale(L.attn.{q,k,v}))
   };
   static constexpr int SMEM_BYTES = 0;
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t*, int) {}
-  template <int BN, int CLUSTER>
+  __device__ static void prologue(const Params&, uint8_t*, int, int) {}
+  template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t*) {
+    // a tile never straddles q|k|v blocks (block_cols % BN == 0)
+    const int blk = c.n0 / p.block_cols;
+    const float mult = blk == 0 ? p.mult0 : blk == 1 ? p.mult1 : p.mult2;
+    const Recip rq = make_recip(blk == 0 ? p.sout0 : blk == 1 ? p.sout1 : p.sout2);
 #pragma unroll 1
-    for (int col = 0; col < BN; col += 32) {
-      const int gcol = c.n0 + col;
-      const int blk = gcol / p.block_cols;
-      const float mult = p.mult[blk], so = p.s_out[blk];
+    for (int col = 0; col < c.ncols; col += 32) {
+      const int gcol = c.n0 + c.c0 + col;
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
+      float b[32];
+      load_bias32(p.bias + gcol, b);
       tmem_wait_ld();
-      uint32_t packed[8];
+      int q[32];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + gcol + j));
-        int q0 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 0])), mult), b.x), so);
-        int q1 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 1])), mult), b.y), so);
-        int q2 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 2])), mult), b.z), so);
-        int q3 = quant_i8(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j + 3])), mult), b.w), so);
-        packed[j / 4] = pack4_i8(q0, q1, q2, q3);
-      }
-      if (c.row < c.M) {
-        uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
-        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-      }
+      for (int j = 0; j < 32; ++j)
+        q[j] = quant_fast(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j])), mult), b[j]), rq);
+      if (c.row < c.M) store32_i8(p.out + size_t(c.row) * p.ldo + gcol, q);
     }
   }
 };
@@ -253,35 +266,82 @@ struct EpiGeluQuant {
   };
   static constexpr int SMEM_BYTES = sizeof(TanhTable);
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t* smem, int tid) {
-    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, 128);
+  __device__ static void prologue(const Params&, uint8_t* smem, int tid, int nthreads) {
+    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nthreads);
   }
-  template <int BN, int CLUSTER>
+  template <int BN, int CLUSTER, int NE>
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
+    const Recip rq = make_recip(p.s_out);
+    // 16 columns per step keeps the 8-wide batched table lookups under the 96-register cap
+#pragma unroll 1
+    for (int col = 0; col < c.ncols; col += 16) {
+      const int gcol = c.n0 + c.c0 + col;
+      uint32_t r[16];
+      tmem_ld16(c.taddr + col, r);
+      float b[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p.bias + gcol) + j);
+        b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
+      }
+      tmem_wait_ld();
+      uint32_t w[4];
+#pragma unroll
+      for (int g = 0; g < 16; g += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
+        gelu8(v, tt);
+        w[g / 4] = pack4_i8(quant_fast(v[0], rq), quant_fast(v[1], rq), quant_fast(v[2], rq), quant_fast(v[3], rq));
+        w[g / 4 + 1] = pack4_i8(quant_fast(v[4], rq), quant_fast(v[5], rq), quant_fast(v[6], rq), quant_fast(v[7], rq));
+      }
+      if (c.row < c.M) *reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+};
+
+// FP16-path bias (+ optional GELU) epilogue: acc(F32) + bias [-> gelu] -> f16 storage.
+// (reference mha_fp encoder.py:291-292 qkv = gemm + qkv_b; ffn_fp :325-326 gelu(mid))
+struct EpiF16Out {
+  struct Params {
+    __half* out;
+    int ldo;
+    const float* bias;
+    int gelu;
+  };
+  static constexpr int SMEM_BYTES = sizeof(TanhTable);
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
+  __device__ static void prologue(const Params&, uint8_t* smem, int tid, int nthreads) {
+    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nthreads);
+  }
+  template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
     const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
 #pragma unroll 1
-    for (int col = 0; col < BN; col += 32) {
-      const int gcol = c.n0 + col;
+    for (int col = 0; col < c.ncols; col += 32) {
+      const int gcol = c.n0 + c.c0 + col;
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
+      float b[32];
+      load_bias32(p.bias + gcol, b);
       tmem_wait_ld();
-      uint32_t packed[8];
+      uint32_t packed[16];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + gcol + j));
-        const float bb[4] = {b.x, b.y, b.z, b.w};
-        int q[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float mid = __fadd_rn(__fmul_rn(__int2float_rn(int(r[j + u])), p.mult), bb[u]);
-          q[u] = quant_i8(gelu_ref(mid, tt), p.s_out);
+      for (int j = 0; j < 32; j += 2) {
+        float x0 = __fadd_rn(__uint_as_float(r[j]), b[j]);
+        float x1 = __fadd_rn(__uint_as_float(r[j + 1]), b[j + 1]);
+        if (p.gelu) {
+          x0 = gelu_ref(x0, tt);
+          x1 = gelu_ref(x1, tt);
         }
-        packed[j / 4] = pack4_i8(q[0], q[1], q[2], q[3]);
+        __half2 h = __floats2half2_rn(x0, x1);
+        packed[j / 2] = *reinterpret_cast<uint32_t*>(&h);
       }
       if (c.row < c.M) {
         uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
-        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
       }
     }
   }
@@ -292,6 +352,8 @@ struct EpiGeluQuant {
 //   out = ((x - mean) * inv) * gamma + beta      mean/var: numpy pairwise over H
 // then any of: int8 quantize(s_out), f32 store, f16 store.
 // (reference encoder.py:381-385 out-proj, :412-418 FFN2; kernels.layernorm :138-154)
+// Sum order: each thread reduces its (half) row = one numpy subtree; the two halves are
+// added (NE == 8), then the CLUSTER CTAs' partials in tree order through DSMEM.
 struct EpiResLN {
   struct Params {
     const float* bias;
@@ -305,29 +367,57 @@ struct EpiResLN {
     float eps;
     int hidden;
     int8_t* out_i8;  float s_out;   // optional
+    int deq_outputs;                // f32/f16 outputs carry F32(q)*s_out (MHA-only layers)
+    int f16_round;                  // reference fp16 storage: round the f32 output through f16
     float* out_f32;                 // optional
     __half* out_f16;                // optional
   };
-  static constexpr int SMEM_BYTES = 2 * 128 * sizeof(float);
+  // [0,256): per-half partials; [256,512): CTA partials for the two cluster exchanges
+  static constexpr int SMEM_BYTES = 4 * 128 * sizeof(float);
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return CLUSTER > 1 ? 2 : 0; }
-  __device__ static void prologue(const Params&, uint8_t*, int) {}
+  __device__ static void prologue(const Params&, uint8_t*, int, int) {}
 
-  template <int BN, int CLUSTER>
+  template <int CLUSTER, int NE>
+  __device__ static float reduce_row(float mine, const EpiCtx& c, float* halves, float* cta) {
+    float s = mine;
+    if constexpr (NE == 8) {
+      halves[c.half * 128 + c.tile_row] = mine;
+      epi_bar_sync(c.ne_threads);
+      s = __fadd_rn(halves[c.tile_row], halves[128 + c.tile_row]);
+    }
+    if constexpr (CLUSTER > 1) {
+      cta[c.tile_row] = s;      // both halves write the same value
+      cluster_sync_all();
+      float p[CLUSTER];
+#pragma unroll
+      for (int r = 0; r < CLUSTER; ++r) p[r] = dsmem_ld_f32(&cta[c.tile_row], r);
+      if constexpr (CLUSTER == 2) s = __fadd_rn(p[0], p[1]);
+      else s = __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
+    } else if constexpr (NE == 8) {
+      epi_bar_sync(c.ne_threads);   // halves[] is reused by the second reduction
+    }
+    return s;
+  }
+
+  template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
-    float* red = reinterpret_cast<float*>(smem);
+    float* halves = reinterpret_cast<float*>(smem);
+    float* cta0 = halves + 256;
+    float* cta1 = cta0 + 128;
     const bool valid = c.row < c.M;
     const size_t rbase = size_t(valid ? c.row : 0) * p.hidden;
+    const int gbase = c.n0 + c.c0;
     // pass 1: x = (acc*mult + b) + residual, written back into TMEM as f32 bits
 #pragma unroll 1
-    for (int col = 0; col < BN; col += 32) {
-      const int gcol = c.n0 + col;
+    for (int col = 0; col < c.ncols; col += 32) {
+      const int gcol = gbase + col;
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
-      tmem_wait_ld();
-      float res[32];
+      float res[32], b[32];
+      load_bias32(p.bias + gcol, b);
       if (p.res_i8) {
         const uint4* src = reinterpret_cast<const uint4*>(p.res_i8 + rbase + gcol);
-        uint4 u0 = src[0], u1 = src[1];
+        const uint4 u0 = src[0], u1 = src[1];
         const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
         for (int j = 0; j < 32; ++j) res[j] = deq(int(int8_t((w[j / 4] >> (8 * (j % 4))) & 0xff)), p.res_scale);
@@ -335,70 +425,92 @@ struct EpiResLN {
         const float4* src = reinterpret_cast<const float4*>(p.res_f32 + rbase + gcol);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float4 v = src[j];
+          const float4 v = src[j];
           res[4 * j] = v.x; res[4 * j + 1] = v.y; res[4 * j + 2] = v.z; res[4 * j + 3] = v.w;
         }
       }
+      tmem_wait_ld();
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float b = __ldg(p.bias + gcol + j);
         const float acc = p.acc_is_f32 ? __uint_as_float(r[j]) : __fmul_rn(__int2float_rn(int(r[j])), p.mult);
-        r[j] = __float_as_uint(__fadd_rn(__fadd_rn(acc, b), res[j]));
+        r[j] = __float_as_uint(__fadd_rn(__fadd_rn(acc, b[j]), res[j]));
       }
       tmem_st32(c.taddr + col, r);
     }
     tmem_wait_st();
 
-    auto get_x = [&](int off, float (&v)[8]) {
-      uint32_t u[8];
-      tmem_ld8(c.taddr + off, u);
-      tmem_wait_ld();
+    // numpy pairwise sum of f(x) over this thread's columns.  A single 32-aligned leaf
+    // (96 / 128 columns for H = 768 / 1024) streams TMEM 32 columns per load; anything
+    // else walks the generic tree 8 columns at a time.
+    auto row_sum = [&](auto f) -> float {
+      if (c.ncols <= 128 && (c.ncols & 31) == 0) {
+        float acc[8];
+#pragma unroll 1
+        for (int col = 0; col < c.ncols; col += 32) {
+          uint32_t u[32];
+          tmem_ld32(c.taddr + col, u);
+          tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(u[j]);
+          for (int g = 0; g < 4; ++g) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float v = f(__uint_as_float(u[8 * g + j]));
+              acc[j] = (col == 0 && g == 0) ? v : __fadd_rn(acc[j], v);
+            }
+          }
+        }
+        return __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                         __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+      }
+      auto get8 = [&](int off, float (&v)[8]) {
+        uint32_t u[8];
+        tmem_ld8(c.taddr + off, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = f(__uint_as_float(u[j]));
+      };
+      return pairwise_sum(c.ncols, get8);
     };
-    float s1 = pairwise_sum(BN, get_x);
-    float total = cluster_tree_sum<CLUSTER>(red, c.ep_tid, s1);
+    const float total = reduce_row<CLUSTER, NE>(row_sum([](float x) { return x; }), c, halves, cta0);
     const float hf = float(p.hidden);
     const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
-
-    auto get_c2 = [&](int off, float (&v)[8]) {
-      uint32_t u[8];
-      tmem_ld8(c.taddr + off, u);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float d = __fsub_rn(__uint_as_float(u[j]), mean);
-        v[j] = __fmul_rn(d, d);
-      }
-    };
-    float s2 = pairwise_sum(BN, get_c2);
-    float total2 = cluster_tree_sum<CLUSTER>(red + 128, c.ep_tid, s2);
+    const float total2 = reduce_row<CLUSTER, NE>(row_sum([mean](float x) {
+                                                   const float d = __fsub_rn(x, mean);
+                                                   return __fmul_rn(d, d);
+                                                 }),
+                                                 c, halves, cta1);
     const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+    const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);
 
     // pass 3: normalise, affine, emit
 #pragma unroll 1
-    for (int col = 0; col < BN; col += 32) {
-      const int gcol = c.n0 + col;
+    for (int col = 0; col < c.ncols; col += 32) {
+      const int gcol = gbase + col;
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
+      float g[32], be[32];
+      load_bias32(p.gamma + gcol, g);
+      load_bias32(p.beta + gcol, be);
       tmem_wait_ld();
       float y[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float g = __ldg(p.gamma + gcol + j), b = __ldg(p.beta + gcol + j);
-        y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(__uint_as_float(r[j]), mean), inv), g), b);
-      }
+      for (int j = 0; j < 32; ++j)
+        y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(__uint_as_float(r[j]), mean), inv), g[j]), be[j]);
       if (!valid) continue;
-      if (p.out_i8) {
-        uint32_t packed[8];
+      if (p.out_i8 || p.deq_outputs) {
+        int q[32];
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          packed[j / 4] = pack4_i8(quant_i8(y[j], p.s_out), quant_i8(y[j + 1], p.s_out),
-                                   quant_i8(y[j + 2], p.s_out), quant_i8(y[j + 3], p.s_out));
-        uint4* dst = reinterpret_cast<uint4*>(p.out_i8 + rbase + gcol);
-        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        for (int j = 0; j < 32; ++j) q[j] = quant_fast(y[j], rq);
+        if (p.out_i8) store32_i8(p.out_i8 + rbase + gcol, q);
+        if (p.deq_outputs) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
+        }
+      }
+      if (p.f16_round) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
       }
       if (p.out_f32) {
         float4* dst = reinterpret_cast<float4*>(p.out_f32 + rbase + gcol);
@@ -419,16 +531,12 @@ struct EpiResLN {
   }
 };
 
-}  // namespace samp
-
 // ------------------------------------------------------------------ host launcher
-namespace samp {
-
-template <int KIND, int BN, int STAGES, int CLUSTER, class Epi>
+template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
 inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N, int k_bytes,
                                const typename Epi::Params& p, cudaStream_t stream) {
   using Lay = GemmLayout<BN, STAGES, Epi::SMEM_BYTES>;
-  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, Epi>;
+  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi>;
   static thread_local int configured_device = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -439,7 +547,7 @@ inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, 1);
-  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+  cfg.blockDim = dim3(64 + 32 * NE, 1, 1);
   cfg.dynamicSmemBytes = Lay::TOTAL;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

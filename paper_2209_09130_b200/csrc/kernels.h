@@ -1,0 +1,43 @@
+// Launch wrappers implemented in separate translation units (parallel compile).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "attention.cuh"
+#include "embed.cuh"
+#include "gemm.cuh"
+#include "heads.cuh"
+
+namespace samp {
+
+struct Tiles {
+  int bn_qkv, bn_ffn1, bn_ln, cluster_ln;
+};
+
+// gemm_i8.cu
+cudaError_t gemm_qkv_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+                        const EpiQKV::Params& p, cudaStream_t st);
+cudaError_t gemm_gelu_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+                         const EpiGeluQuant::Params& p, cudaStream_t st);
+// gemm_ln.cu
+cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+                       const EpiResLN::Params& p, cudaStream_t st);
+cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+                        const EpiResLN::Params& p, cudaStream_t st);
+// gemm_f16.cu
+cudaError_t gemm_f16out(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+                        const EpiF16Out::Params& p, cudaStream_t st);
+// attention.cu
+cudaError_t launch_attention_i8(const CUtensorMap& map, const AttnParams& p, int ntiles, int heads, int keys_cap,
+                                cudaStream_t st);
+cudaError_t launch_attention_f16(const CUtensorMap& map, const AttnParams& p, int ntiles, int heads, int keys_cap,
+                                 cudaStream_t st);
+// misc_kernels.cu
+cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st);
+cudaError_t launch_classify(const HeadParams& p, cudaStream_t st);
+cudaError_t launch_tag(const HeadParams& p, cudaStream_t st);
+cudaError_t launch_pack_weight(const float* w, int K, int N, float scale, int8_t* out_i8, __half* out_f16,
+                               int row_off, cudaStream_t st);
+cudaError_t launch_transpose_f32(const float* w, int K, int N, float* out, cudaStream_t st);
+
+}  // namespace samp

@@ -1,0 +1,86 @@
+// Embedding, heads, and load-time weight packing kernels.
+#define SAMP_DEFINE_KERNELS
+#include "kernels.h"
+
+namespace samp {
+
+cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaError_t e = cudaFuncSetAttribute(embed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = dev;
+  }
+  const size_t smem = size_t(EMB_TOK) * (p.hidden + EMB_PAD) * sizeof(float);
+  embed_kernel<<<(p.T + EMB_TOK - 1) / EMB_TOK, EMB_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_classify(const HeadParams& p, cudaStream_t st) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaError_t e = cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = dev;
+  }
+  const dim3 grid((p.hidden_size + POOL_COLS - 1) / POOL_COLS, (p.nseq + POOL_SEQS - 1) / POOL_SEQS);
+  pooler_kernel<<<grid, HEAD_THREADS, (size_t(POOL_SEQS) * p.hidden_size + 8 * POOL_SEQS * 32) * sizeof(float), st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  classifier_kernel<<<(p.nseq + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32), HEAD_THREADS, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tag(const HeadParams& p, cudaStream_t st) {
+  tag_kernel<<<(p.T + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32), HEAD_THREADS, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// W [K][N] F32 (archive layout) -> Wt int8 [N][K] (one per-tensor scale, reference
+// quantize_weight encoder.py:191-194) and Wt f16 [N][K]; rows land at `row_off`.
+__global__ void pack_weight_kernel(const float* __restrict__ w, int K, int N, float scale,
+                                   int8_t* __restrict__ out_i8, __half* __restrict__ out_f16, int row_off) {
+  __shared__ float tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx over N, by over K
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int k = by + i, n = bx + threadIdx.x;
+    if (k < K && n < N) tile[i][threadIdx.x] = w[size_t(k) * N + n];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int n = bx + i, k = by + threadIdx.x;
+    if (k < K && n < N) {
+      const float v = tile[threadIdx.x][i];
+      const size_t o = size_t(row_off + n) * K + k;
+      out_i8[o] = int8_t(quant_i8(v, scale));
+      out_f16[o] = __float2half_rn(v);
+    }
+  }
+}
+
+cudaError_t launch_pack_weight(const float* w, int K, int N, float scale, int8_t* out_i8, __half* out_f16,
+                               int row_off, cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+  pack_weight_kernel<<<grid, block, 0, st>>>(w, K, N, scale, out_i8, out_f16, row_off);
+  return cudaGetLastError();
+}
+
+__global__ void transpose_f32_kernel(const float* __restrict__ w, int K, int N, float* __restrict__ out) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < size_t(K) * N) {
+    const int k = int(i / N), n = int(i % N);
+    out[size_t(n) * K + k] = w[i];
+  }
+}
+
+cudaError_t launch_transpose_f32(const float* w, int K, int N, float* out, cudaStream_t st) {
+  const size_t n = size_t(K) * N;
+  transpose_f32_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(w, K, N, out);
+  return cudaGetLastError();
+}
+
+}  // namespace samp

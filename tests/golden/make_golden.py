@@ -137,5 +137,28 @@ def main():
               taps_plan=("FULLY_QUANT", 1))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def bench_calibration(model="bert-base", n_seq=8, seq=128):
+    """Reference Engine.calibrate for the bench model (SURVEY.md §8(d) recipe):
+    BERT-shaped random init (seed 0, weight_scale 0.02, vocab 30522, max_position 512),
+    8 default_rng(1) sequences of 128 ids, FP32 plan.  Written to bench_calibration_<model>.json."""
+    from samp.synthetic import build_archive as ref_build
+    shapes = {"bert-base": dict(num_layers=12, hidden=768, num_heads=12, intermediate=3072),
+              "bert-large": dict(num_layers=24, hidden=1024, num_heads=16, intermediate=4096)}[model]
+    vocab = tiny_vocab(max_seq_len=512, extra_tokens=[f"[unused{i}]" for i in range(30522 - 44)])
+    arch = ref_build(task="classification", num_labels=2, max_position=512, seed=0, weight_scale=0.02,
+                     vocab=vocab, **shapes)
+    rng = np.random.default_rng(1)
+    encs = [EncodedInput(rng.integers(0, 30522, size=seq).tolist(), [0] * seq, seq) for _ in range(n_seq)]
+    table = Engine(arch).calibrate(encs)
+    path = os.path.join(HERE, f"bench_calibration_{model}.json")
+    with open(path, "w") as fh:
+        fh.write(table.to_json() + "\n")
+    print("wrote", path, len(table.entries), "sites")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--bench-calibration":
+    bench_calibration(*(sys.argv[2:3] or ["bert-base"]))

@@ -51,3 +51,65 @@ def test_gemm_f16(m, n, k):
     _lib.check(lib.samp_debug_gemm_f16(_lib.ptr(a.view(np.uint16)), _lib.ptr(b.view(np.uint16)), _lib.ptr(c), m, n, k))
     want = a.astype(np.float64) @ b.astype(np.float64)
     np.testing.assert_allclose(c, want, rtol=1e-3, atol=1e-3)
+
+
+def _scales_from_bench():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "bench_calibration_bert-base.json")
+    amax = [v["amax"] for v in json.load(open(path))["sites"].values()]
+    s = [float(np.float32(max(a, 127e-8) / 127.0)) for a in amax]
+    rng = np.random.default_rng(0)
+    s += list(np.float32(10.0 ** rng.uniform(-8, 2, 24)))
+    s += [1.0, 0.5, 1 / 127, 2.0 ** -20, 3.0]
+    return np.array(s, np.float32)
+
+
+def test_quantize_fast_path_exhaustive():
+    """quant_fast == quantize with the IEEE divide for every float x and 130 scales (all
+    bench-calibration site scales + random ones): 5.6e11 comparisons on the device."""
+    import ctypes
+    lib = _lib.load()
+    s = _scales_from_bench()
+    bad = ctypes.c_ulonglong()
+    _lib.check(lib.samp_debug_quant_exhaustive(_lib.ptr(s), len(s), ctypes.byref(bad)))
+    assert bad.value == 0
+
+
+def test_division_fast_path_exhaustive():
+    import ctypes
+    lib = _lib.load()
+    d = np.concatenate([_scales_from_bench()[:40], np.array([1.0, 1.5, 7.0, 128.0, 511.9, 333.3], np.float32)])
+    bad = ctypes.c_ulonglong()
+    _lib.check(lib.samp_debug_div_exhaustive(_lib.ptr(d), len(d), ctypes.byref(bad)))
+    assert bad.value == 0
+
+
+def test_exp_fast_division_exhaustive():
+    import ctypes
+    lib = _lib.load()
+    bad = ctypes.c_ulonglong()
+    _lib.check(lib.samp_debug_exp_exhaustive(ctypes.byref(bad)))
+    assert bad.value == 0
+
+
+@pytest.mark.parametrize("fn,name", [(0, "np_exp"), (1, "np_tanh")])
+def test_device_transcendentals_equal_oracle(fn, name):
+    lib = _lib.load()
+    rng = np.random.default_rng(fn)
+    x = np.concatenate([rng.integers(0, 2**32, 1 << 22, dtype=np.uint64).astype(np.uint32).view(np.float32),
+                        rng.uniform(-104, 1, 1 << 21).astype(np.float32),
+                        rng.uniform(-10, 10, 1 << 21).astype(np.float32)])
+    y = np.empty_like(x)
+    _lib.check(lib.samp_debug_unary(fn, _lib.ptr(x), _lib.ptr(y), x.size))
+    want = getattr(orc, name)(x)
+    same = (want.view(np.uint32) == y.view(np.uint32)) | (np.isnan(want) & np.isnan(y))
+    assert same.all(), f"{np.count_nonzero(~same)} mismatches"
+
+
+def test_device_gelu_equals_oracle():
+    lib = _lib.load()
+    x = np.random.default_rng(9).standard_normal(1 << 22).astype(np.float32) * 4
+    y = np.empty_like(x)
+    _lib.check(lib.samp_debug_unary(2, _lib.ptr(x), _lib.ptr(y), x.size))
+    np.testing.assert_array_equal(y, orc.gelu(x))

@@ -76,7 +76,7 @@ struct AttnLayout {
 __device__ __forceinline__ void att_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <bool F16>
-__global__ void __launch_bounds__(ATT_THREADS)
+__global__ void __launch_bounds__(ATT_THREADS, 3)
 attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p, int keys_cap) {
   using C = AttnCfg<F16>;
   extern __shared__ uint8_t smem_raw[];

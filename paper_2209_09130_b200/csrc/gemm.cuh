@@ -69,11 +69,17 @@ __device__ __forceinline__ void epi_bar_sync(int nthreads) {
   asm volatile("bar.sync 1, %0;" :: "r"(nthreads) : "memory");
 }
 
+// rings <= ~110 KB run two CTAs per SM (register cap ~96); deeper rings one CTA per SM
+template <int BN, int STAGES>
+struct GemmOcc {
+  static constexpr int value = STAGES * (GEMM_BM + BN) * 128 <= 110 * 1024 ? 2 : 1;
+};
+
 template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
-__global__ void __launch_bounds__(64 + 32 * NE, 2)
+__global__ void __launch_bounds__(64 + 32 * NE, GemmOcc<BN, STAGES>::value)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             int M, int k_bytes, const typename Epi::Params ep) {
-  using Lay = GemmLayout<BN, STAGES, Epi::SMEM_BYTES>;
+  using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
   constexpr int TMEM_COLS = tmem_cols_for(BN);
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -107,7 +113,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     tma_prefetch(&map_b);
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
-  if (warp >= GEMM_EPI_WARP0) Epi::prologue(ep, epi_smem, threadIdx.x - GEMM_EPI_WARP0 * 32, 32 * NE);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -150,6 +155,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     const int half = NE == 8 ? int(warp - GEMM_EPI_WARP0) / 4 : 0;
     const int tile_row = quarter * 32 + lane_id();
     const int c0 = half * (BN / (NE / 4));
+    // idle during the main loop: stage this tile's epilogue operands in smem
+    Epi::template prefetch<BN>(ep, epi_smem, m0, n0, M, ep_tid, 32 * NE);
+    epi_bar_sync(32 * NE);
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(c0), m0 + tile_row, tile_row, n0, c0,
@@ -190,7 +198,22 @@ __device__ __forceinline__ void load_bias32(const float* b, float (&out)[32]) {
   }
 }
 
+__device__ __forceinline__ void load_smem32(const float* src, float (&out)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = reinterpret_cast<const float4*>(src)[j];
+    out[4 * j] = v.x; out[4 * j + 1] = v.y; out[4 * j + 2] = v.z; out[4 * j + 3] = v.w;
+  }
+}
+
+// copy n floats gmem -> smem cooperatively
+__device__ __forceinline__ void stage_floats(float* dst, const float* src, int n, int tid, int nthreads) {
+  for (int i = tid; i < n; i += nthreads) dst[i] = __ldg(src + i);
+}
+
 // ------------------------------------------------------------------ epilogues
+// Interface: smem_bytes<BN>(); prefetch<BN>(params, smem, m0, n0, M, tid, nthreads) runs in
+// the epilogue warps while the main loop is in flight; run<BN, CLUSTER, NE>(params, ctx, smem).
 
 // raw int32 / f32 accumulator store (kernel tests, parity of the accumulators)
 struct EpiStoreAcc {
@@ -198,9 +221,9 @@ struct EpiStoreAcc {
     void* out;   // int32 (kind::i8) or float (kind::f16), row-major
     int ldc;     // elements
   };
-  static constexpr int SMEM_BYTES = 0;
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return 0; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t*, int, int) {}
+  template <int BN> __device__ static void prefetch(const Params&, uint8_t*, int, int, int, int, int) {}
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t*) {
 #pragma unroll 1
@@ -228,11 +251,15 @@ struct EpiQKV {
     float mult0, mult1, mult2;     // F32(double(s_in) * double(s_w{q,k,v}))
     float sout0, sout1, sout2;     // F32(scale(L.attn.{q,k,v}))
   };
-  static constexpr int SMEM_BYTES = 0;
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return BN * 4; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t*, int, int) {}
+  template <int BN>
+  __device__ static void prefetch(const Params& p, uint8_t* smem, int, int n0, int, int tid, int nt) {
+    stage_floats(reinterpret_cast<float*>(smem), p.bias + n0, BN, tid, nt);
+  }
   template <int BN, int CLUSTER, int NE>
-  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t*) {
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    const float* sbias = reinterpret_cast<const float*>(smem);
     // a tile never straddles q|k|v blocks (block_cols % BN == 0)
     const int blk = c.n0 / p.block_cols;
     const float mult = blk == 0 ? p.mult0 : blk == 1 ? p.mult1 : p.mult2;
@@ -243,7 +270,7 @@ struct EpiQKV {
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
       float b[32];
-      load_bias32(p.bias + gcol, b);
+      load_smem32(sbias + c.c0 + col, b);
       tmem_wait_ld();
       int q[32];
 #pragma unroll
@@ -264,14 +291,17 @@ struct EpiGeluQuant {
     float mult;
     float s_out;
   };
-  static constexpr int SMEM_BYTES = sizeof(TanhTable);
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t* smem, int tid, int nthreads) {
-    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nthreads);
+  template <int BN>
+  __device__ static void prefetch(const Params& p, uint8_t* smem, int, int n0, int, int tid, int nt) {
+    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nt);
+    stage_floats(reinterpret_cast<float*>(smem + sizeof(TanhTable)), p.bias + n0, BN, tid, nt);
   }
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
     const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
+    const float* sbias = reinterpret_cast<const float*>(smem + sizeof(TanhTable));
     const Recip rq = make_recip(p.s_out);
     // 16 columns per step keeps the 8-wide batched table lookups under the 96-register cap
 #pragma unroll 1
@@ -282,7 +312,7 @@ struct EpiGeluQuant {
       float b[16];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(p.bias + gcol) + j);
+        const float4 v = reinterpret_cast<const float4*>(sbias + c.c0 + col)[j];
         b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
       }
       tmem_wait_ld();
@@ -310,21 +340,24 @@ struct EpiF16Out {
     const float* bias;
     int gelu;
   };
-  static constexpr int SMEM_BYTES = sizeof(TanhTable);
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
-  __device__ static void prologue(const Params&, uint8_t* smem, int tid, int nthreads) {
-    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nthreads);
+  template <int BN>
+  __device__ static void prefetch(const Params& p, uint8_t* smem, int, int n0, int, int tid, int nt) {
+    load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nt);
+    stage_floats(reinterpret_cast<float*>(smem + sizeof(TanhTable)), p.bias + n0, BN, tid, nt);
   }
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
     const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
+    const float* sbias = reinterpret_cast<const float*>(smem + sizeof(TanhTable));
 #pragma unroll 1
     for (int col = 0; col < c.ncols; col += 32) {
       const int gcol = c.n0 + c.c0 + col;
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
       float b[32];
-      load_bias32(p.bias + gcol, b);
+      load_smem32(sbias + c.c0 + col, b);
       tmem_wait_ld();
       uint32_t packed[16];
 #pragma unroll
@@ -372,10 +405,33 @@ struct EpiResLN {
     float* out_f32;                 // optional
     __half* out_f16;                // optional
   };
-  // [0,256): per-half partials; [256,512): CTA partials for the two cluster exchanges
-  static constexpr int SMEM_BYTES = 4 * 128 * sizeof(float);
+  // smem: [0,512) floats reduction scratch (per-half partials, 2 x CTA partials), then
+  // bias / gamma / beta slices (BN floats each), then the int8 residual tile
+  // [128][BN + 16] (16-byte row pad: conflict-free 16 B reads by consecutive rows)
+  static constexpr int RED_FLOATS = 4 * 128;
+  template <int BN> __host__ __device__ static constexpr int res_ld() { return BN + 16; }
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() {
+    return (RED_FLOATS + 3 * BN) * 4 + 128 * res_ld<BN>();
+  }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return CLUSTER > 1 ? 2 : 0; }
-  __device__ static void prologue(const Params&, uint8_t*, int, int) {}
+  template <int BN>
+  __device__ static void prefetch(const Params& p, uint8_t* smem, int m0, int n0, int M, int tid, int nt) {
+    float* f = reinterpret_cast<float*>(smem) + RED_FLOATS;
+    stage_floats(f, p.bias + n0, BN, tid, nt);
+    stage_floats(f + BN, p.gamma + n0, BN, tid, nt);
+    stage_floats(f + 2 * BN, p.beta + n0, BN, tid, nt);
+    if (p.res_i8) {
+      uint8_t* rt = smem + (RED_FLOATS + 3 * BN) * 4;
+      constexpr int V = BN / 16;  // uint4 per row
+      for (int i = tid; i < 128 * V; i += nt) {
+        const int row = i / V, v = i % V;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (m0 + row < M)
+          val = __ldg(reinterpret_cast<const uint4*>(p.res_i8 + size_t(m0 + row) * p.hidden + n0) + v);
+        *reinterpret_cast<uint4*>(rt + row * res_ld<BN>() + v * 16) = val;
+      }
+    }
+  }
 
   template <int CLUSTER, int NE>
   __device__ static float reduce_row(float mine, const EpiCtx& c, float* halves, float* cta) {
@@ -404,6 +460,10 @@ struct EpiResLN {
     float* halves = reinterpret_cast<float*>(smem);
     float* cta0 = halves + 256;
     float* cta1 = cta0 + 128;
+    const float* sbias = halves + RED_FLOATS;
+    const float* sgam = sbias + BN;
+    const float* sbet = sgam + BN;
+    const uint8_t* rtile = smem + (RED_FLOATS + 3 * BN) * 4 + c.tile_row * res_ld<BN>();
     const bool valid = c.row < c.M;
     const size_t rbase = size_t(valid ? c.row : 0) * p.hidden;
     const int gbase = c.n0 + c.c0;
@@ -414,9 +474,9 @@ struct EpiResLN {
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
       float res[32], b[32];
-      load_bias32(p.bias + gcol, b);
+      load_smem32(sbias + c.c0 + col, b);
       if (p.res_i8) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.res_i8 + rbase + gcol);
+        const uint4* src = reinterpret_cast<const uint4*>(rtile + c.c0 + col);
         const uint4 u0 = src[0], u1 = src[1];
         const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
@@ -490,8 +550,8 @@ struct EpiResLN {
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
       float g[32], be[32];
-      load_bias32(p.gamma + gcol, g);
-      load_bias32(p.beta + gcol, be);
+      load_smem32(sgam + c.c0 + col, g);
+      load_smem32(sbet + c.c0 + col, be);
       tmem_wait_ld();
       float y[32];
 #pragma unroll
@@ -535,7 +595,7 @@ struct EpiResLN {
 template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
 inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N, int k_bytes,
                                const typename Epi::Params& p, cudaStream_t stream) {
-  using Lay = GemmLayout<BN, STAGES, Epi::SMEM_BYTES>;
+  using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
   auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi>;
   static thread_local int configured_device = -1;
   int dev = 0;

@@ -28,6 +28,9 @@ def __getattr__(name):
                 "select_by_accuracy_threshold", "select_by_latency_threshold"):
         from . import allocator
         return getattr(allocator, name)
+    if name in ("trace_ops",):
+        from . import trace
+        return trace.trace_ops
     raise AttributeError(name)
 
 

@@ -25,6 +25,7 @@ from .errors import CalibrationError, ConfigurationError, InputError
 from .plan import (EMBED_OUT_SITE, LAYER_CODE, LAYER_FP, PrecisionPlan)
 from .quantization import CalibrationTable, QuantScale, quantize
 from .tokenization import EncodedInput, encode as encode_text
+from . import trace as _trace
 
 HEAD_NONE, HEAD_CLASSIFY, HEAD_TAG = 0, 1, 2
 IO_HOST, IO_DEVICE = 0, 1
@@ -197,10 +198,19 @@ class Engine:
         segs = np.concatenate([np.asarray(e.segment_ids, dtype=np.int32) for e in encs])
         return seq_start, att, ids, segs
 
+    def _trace(self, plan: PrecisionPlan, seq_start) -> None:
+        tr = _trace.active()
+        if tr is not None:
+            m = self.manifest
+            for s in range(len(seq_start) - 1):
+                _trace.record_forward(tr, plan.layer_precisions, int(seq_start[s + 1] - seq_start[s]),
+                                      m.hidden, m.num_heads, m.intermediate)
+
     def forward_packed(self, plan: PrecisionPlan, seq_start, att_len, ids, segs, *, hidden=True,
                        head: int | None = None) -> BatchOutput:
         """One samp_forward call over packed host arrays (validated by the library)."""
         self.check_plan(plan)
+        self._trace(plan, seq_start)
         self._push_calibration()
         m = self.manifest
         nseq = len(seq_start) - 1

@@ -3,14 +3,14 @@
 // Reference: encoder.embed_fused (pkg/src/samp/encoder.py:249-273) and the first
 // FULL_INT8 layer's quantize (encoder.py:505-510).
 //
-// One 8-lane group per token (4 tokens per warp, 32 per 256-thread block).
-//   gather:  the group sums ((word + pos) + type) in reference order with float4 loads
-//            (all rows of the block in flight at once) into a padded smem row;
-//   LN:      numpy's pairwise tree over H, cooperatively: inside a leaf, lane j owns the
-//            j-th of the 8 strided accumulators (exactly numpy's r[j] chains), the
-//            ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) combine is an xor-butterfly (IEEE add is
-//            commutative, the pairing is numpy's), tails and the tree above the leaves are
-//            evaluated identically by all 8 lanes;
+// One warp per token (8 tokens per 256-thread block).
+//   gather:  lanes sum ((word + pos) + type) in reference order with float4 loads into a
+//            smem row;
+//   LN:      numpy's pairwise tree over H (pairwise_warp): the tree's leaves are shared
+//            out to four 8-lane groups; inside a leaf lane j owns the j-th of numpy's 8
+//            strided accumulators, the ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) combine is an
+//            xor-butterfly (IEEE add is commutative, the pairing is numpy's), tails and
+//            the tree above the leaves are evaluated identically by every lane;
 //   emit:    normalise + every requested output.
 #pragma once
 #include <cuda_fp16.h>
@@ -19,9 +19,7 @@
 
 namespace samp {
 
-constexpr int EMB_TOK = 32;        // tokens per block
-constexpr int EMB_THREADS = 256;   // 8 lanes per token
-constexpr int EMB_PAD = 8;         // row padding (floats): groups of a warp hit distinct banks
+constexpr int EMB_THREADS = 256;   // one warp per token, 8 tokens per block
 
 struct EmbedParams {
   const int* ids;
@@ -92,48 +90,88 @@ __device__ __forceinline__ float pairwise_coop8(int n, int g, V& v) {
 }
 
 #ifdef SAMP_DEFINE_KERNELS  // kernel bodies live in misc_kernels.cu only
+// numpy pairwise sum over row[0, H) by a full warp, H compile-time: leaf l is reduced by
+// the 8-lane group l % 4 (lane j of the group owns numpy's j-th strided accumulator, the
+// xor-butterfly is numpy's ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), tails are added in order),
+// then every lane combines the leaf sums up the (compile-time) tree.
+template <int H, int LI, int PER, class V>
+__device__ __forceinline__ void warp_leaves(float (&mine)[PER], int grp, int g, V& v) {
+  if constexpr (LI < ct_leaves(H)) {
+    constexpr int lo = ct_leaf_lo(H, LI), len = ct_leaf_n(H, LI);
+    constexpr int body = len >= 8 ? len - (len & 7) : 0;
+    if (grp == LI % 4) {
+      const unsigned m = 0xffu << (8 * (LI % 4));
+      float acc = 0.0f;
+      if constexpr (len >= 8) {
+        acc = v(lo + g);
+#pragma unroll
+        for (int i = 8; i < body; i += 8) acc = __fadd_rn(acc, v(lo + i + g));
+        acc = __fadd_rn(acc, __shfl_xor_sync(m, acc, 1));
+        acc = __fadd_rn(acc, __shfl_xor_sync(m, acc, 2));
+        acc = __fadd_rn(acc, __shfl_xor_sync(m, acc, 4));
+      }
+#pragma unroll
+      for (int i = body; i < len; ++i) acc = __fadd_rn(acc, v(lo + i));
+      mine[LI / 4] = acc;
+    }
+    warp_leaves<H, LI + 1, PER>(mine, grp, g, v);
+  }
+}
+
+template <int H, class V>
+__device__ __forceinline__ float pairwise_warp(V& v) {
+  constexpr int PER = (ct_leaves(H) + 3) / 4;
+  const int lane = threadIdx.x & 31;
+  float mine[PER];
+#pragma unroll
+  for (int t = 0; t < PER; ++t) mine[t] = 0.0f;
+  warp_leaves<H, 0, PER>(mine, lane >> 3, lane & 7, v);
+  auto leafval = [&](int li) { return __shfl_sync(0xffffffffu, mine[li >> 2], (li & 3) * 8); };
+  return ct_combine<H, 0>(leafval);
+}
+
+template <int H>
 static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedParams p) {
-  extern __shared__ float xs[];              // [EMB_TOK][H + EMB_PAD]
-  const int H = p.hidden, ld = H + EMB_PAD;
-  const int tok = threadIdx.x >> 3, g = threadIdx.x & 7;
-  const int t = blockIdx.x * EMB_TOK + tok;
-  const bool live = t < p.T;
-  float* row = xs + tok * ld;
-  if (live) {
+  extern __shared__ float xs[];              // [8 warps][H]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (EMB_THREADS / 32) + warp;
+  if (t >= p.T) return;                       // warp-uniform
+  float* row = xs + warp * H;
+  {
     const float* w = p.word + size_t(p.ids[t]) * H;
     const float* ps = p.position + size_t(p.pos[t]) * H;
     const float* ty = p.token_type + size_t(p.segs[t]) * H;
-#pragma unroll 4
-    for (int c = g * 4; c < H; c += 32) {
+#pragma unroll 6
+    for (int c = lane * 4; c < H; c += 128) {
       const float4 a = __ldg(reinterpret_cast<const float4*>(w + c));
       const float4 b = __ldg(reinterpret_cast<const float4*>(ps + c));
       const float4 d = __ldg(reinterpret_cast<const float4*>(ty + c));
-      row[c] = __fadd_rn(__fadd_rn(a.x, b.x), d.x);
-      row[c + 1] = __fadd_rn(__fadd_rn(a.y, b.y), d.y);
-      row[c + 2] = __fadd_rn(__fadd_rn(a.z, b.z), d.z);
-      row[c + 3] = __fadd_rn(__fadd_rn(a.w, b.w), d.w);
+      *reinterpret_cast<float4*>(row + c) = make_float4(
+          __fadd_rn(__fadd_rn(a.x, b.x), d.x), __fadd_rn(__fadd_rn(a.y, b.y), d.y),
+          __fadd_rn(__fadd_rn(a.z, b.z), d.z), __fadd_rn(__fadd_rn(a.w, b.w), d.w));
     }
   }
   __syncwarp();
-  // every lane of the warp runs the (token-uniform) tree; dead tokens read zeros
-  auto vx = [&](int i) { return live ? row[i] : 0.0f; };
+  auto vx = [&](int i) { return row[i]; };
   const float hf = float(H);
-  const float mean = __fdiv_rn(__fadd_rn(0.0f, pairwise_coop8(H, g, vx)), hf);
+  const float mean = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp<H>(vx)), hf);
   auto vc = [&](int i) {
-    const float d = live ? __fsub_rn(row[i], mean) : 0.0f;
+    const float d = __fsub_rn(row[i], mean);
     return __fmul_rn(d, d);
   };
-  const float var = __fdiv_rn(__fadd_rn(0.0f, pairwise_coop8(H, g, vc)), hf);
+  const float var = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp<H>(vc)), hf);
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
-  if (!live) return;
   const Recip rq = make_recip(p.out_i8 ? p.s_out : 1.0f);
   const size_t base = size_t(t) * H;
-  for (int c = g * 4; c < H; c += 32) {
+  for (int c = lane * 4; c < H; c += 128) {
+    const float4 xv = *reinterpret_cast<const float4*>(row + c);
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(p.beta + c));
+    const float xx[4] = {xv.x, xv.y, xv.z, xv.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
     float y[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      y[u] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(row[c + u], mean), inv), __ldg(p.gamma + c + u)),
-                       __ldg(p.beta + c + u));
+      y[u] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xx[u], mean), inv), gg[u]), bb[u]);
       if (p.f16_round) y[u] = __half2float(__float2half_rn(y[u]));
     }
     if (p.out_f32) *reinterpret_cast<float4*>(p.out_f32 + base + c) = make_float4(y[0], y[1], y[2], y[3]);
@@ -143,9 +181,9 @@ static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedPa
           make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
     }
     if (p.out_i8) {
-      const uint32_t w = (uint32_t(quant_fast(y[0], rq)) & 0xff) | ((uint32_t(quant_fast(y[1], rq)) & 0xff) << 8) |
-                         ((uint32_t(quant_fast(y[2], rq)) & 0xff) << 16) | (uint32_t(quant_fast(y[3], rq)) << 24);
-      *reinterpret_cast<uint32_t*>(p.out_i8 + base + c) = w;
+      const uint32_t wv = (uint32_t(quant_fast(y[0], rq)) & 0xff) | ((uint32_t(quant_fast(y[1], rq)) & 0xff) << 8) |
+                          ((uint32_t(quant_fast(y[2], rq)) & 0xff) << 16) | (uint32_t(quant_fast(y[3], rq)) << 24);
+      *reinterpret_cast<uint32_t*>(p.out_i8 + base + c) = wv;
     }
   }
 }

@@ -171,7 +171,7 @@ static void ensure_activations(samp_engine* e, int T) {
   a.logits = e->mem.alloc<float>(size_t(cap) * L);
   a.probs = e->mem.alloc<float>(size_t(cap) * L);
   a.labels = e->mem.alloc<int>(cap);
-  a.pooled = e->mem.alloc<float>(size_t(cap) * H);
+  a.pooled = e->mem.alloc<float>(size_t(POOL_KSPLIT) * cap * H);
   a.cap = cap;
   // GEMM A operands: K-major rows, 128-byte boxes, 128 rows
   a.a_xq[0] = tmap_i8(a.xq[0], cap, H, H, 128, 128);

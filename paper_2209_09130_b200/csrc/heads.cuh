@@ -18,7 +18,8 @@ namespace samp {
 constexpr int HEAD_THREADS = 256;
 constexpr int HEAD_MAX_LABELS = 64;
 constexpr int POOL_COLS = 32;      // output columns per pooler CTA
-constexpr int POOL_SEQS = 32;      // sequences per pooler CTA (8 warps x 4)
+constexpr int POOL_SEQS = 32;      // sequences per pooler CTA
+constexpr int POOL_KSPLIT = 4;     // K quarters (grid.z)
 
 struct HeadParams {
   const float* hidden;     // [T][H]
@@ -27,7 +28,7 @@ struct HeadParams {
   const float* pool_b;     // [H]
   const float* head_wt;    // [L][H] (out, in)
   const float* head_b;     // [L]
-  float* pooled;           // [nseq][H] scratch
+  float* pooled;           // [POOL_KSPLIT][nseq][H] scratch (partial pooler sums)
   int hidden_size, num_labels, nseq, T;
   float* logits;           // classify [nseq][L], tag [T][L]
   float* probs;
@@ -71,36 +72,37 @@ __device__ __forceinline__ void softmax_argmax(const float* lg, float* pr, int* 
   *label = best;
 }
 
-// CTA = 32 output columns x up to 32 sequences; warp w reduces the K slice
-// [w*H/8, (w+1)*H/8) for all sequences (lane = column, 32 independent accumulators),
-// partial sums are combined across warps in a fixed order.
+// pooler_kernel: CTA (x, y, z) = 32 output columns x up to 32 sequences x K-quarter z;
+// warp w reduces K rows [z*H/4 + w*H/32, ...) for all its sequences (lane = column, 32
+// independent accumulators); the 8 warp partials are added in a fixed order and written
+// to pooled[z][s][j].  classifier_kernel (one warp per sequence) adds the 4 quarters in
+// order, applies bias + numpy tanh, then the classifier dot products + exact softmax.
 static __global__ void __launch_bounds__(HEAD_THREADS) pooler_kernel(const HeadParams p) {
-  extern __shared__ float sh[];           // h [POOL_SEQS][H] then partials [8][POOL_SEQS][32]
-  __shared__ TanhTable tt;
-  const int H = p.hidden_size;
+  extern __shared__ float sh[];           // h [POOL_SEQS][H/4] then partials [8][POOL_SEQS][32]
+  const int H = p.hidden_size, KQ = H / POOL_KSPLIT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * POOL_COLS + lane;
   const int s0 = blockIdx.y * POOL_SEQS;
+  const int k_base = blockIdx.z * KQ;
   const int ns = min(POOL_SEQS, p.nseq - s0);
   float* hs = sh;
-  float* part = sh + POOL_SEQS * H;
-  load_tanh_table(&tt, threadIdx.x, HEAD_THREADS);
-  for (int s = warp; s < ns; s += HEAD_THREADS / 32) {      // [CLS] row of each sequence
-    const float4* src = reinterpret_cast<const float4*>(p.hidden + size_t(p.seq_start[s0 + s]) * H);
-    for (int k = lane; k < H / 4; k += 32) reinterpret_cast<float4*>(hs + s * H)[k] = src[k];
+  float* part = sh + POOL_SEQS * KQ;
+  for (int s = warp; s < ns; s += HEAD_THREADS / 32) {      // [CLS] row slices
+    const float* src = p.hidden + size_t(p.seq_start[s0 + s]) * H + k_base;
+    for (int k = lane; k < KQ; k += 32) hs[s * KQ + k] = src[k];
   }
   __syncthreads();
   float acc[POOL_SEQS];
 #pragma unroll
   for (int s = 0; s < POOL_SEQS; ++s) acc[s] = 0.0f;
-  const int k_per = H / (HEAD_THREADS / 32);
+  const int k_per = KQ / (HEAD_THREADS / 32);
   const int k0 = warp * k_per;
   if (j < H) {
 #pragma unroll 4
     for (int k = k0; k < k0 + k_per; ++k) {
-      const float wk = __ldg(p.pool_w + size_t(k) * H + j);
+      const float wk = __ldg(p.pool_w + size_t(k_base + k) * H + j);
 #pragma unroll
-      for (int s = 0; s < POOL_SEQS; ++s) acc[s] = __fmaf_rn(hs[s * H + k], wk, acc[s]);
+      for (int s = 0; s < POOL_SEQS; ++s) acc[s] = __fmaf_rn(hs[s * KQ + k], wk, acc[s]);
     }
   }
 #pragma unroll
@@ -110,18 +112,29 @@ static __global__ void __launch_bounds__(HEAD_THREADS) pooler_kernel(const HeadP
     if (j >= H) continue;
     float v = 0.0f;
     for (int w = 0; w < HEAD_THREADS / 32; ++w) v = __fadd_rn(v, part[(w * POOL_SEQS + s) * 32 + lane]);
-    p.pooled[size_t(s0 + s) * H + j] = np_tanhf(__fadd_rn(v, p.pool_b[j]), &tt);
+    p.pooled[(size_t(blockIdx.z) * p.nseq + s0 + s) * H + j] = v;
   }
 }
 
 static __global__ void __launch_bounds__(HEAD_THREADS) classifier_kernel(const HeadParams p) {
+  extern __shared__ float pooled_s[];     // [8 warps][H]
+  __shared__ TanhTable tt;
   const int H = p.hidden_size, L = p.num_labels;
-  const int s = blockIdx.x * (HEAD_THREADS / 32) + threadIdx.x / 32;
+  load_tanh_table(&tt, threadIdx.x, HEAD_THREADS);
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int s = blockIdx.x * (HEAD_THREADS / 32) + warp;
   if (s >= p.nseq) return;
-  const float* x = p.pooled + size_t(s) * H;
+  float* x = pooled_s + warp * H;
+  for (int k = lane; k < H; k += 32) {
+    float v = p.pooled[size_t(s) * H + k];
+    for (int z = 1; z < POOL_KSPLIT; ++z) v = __fadd_rn(v, p.pooled[(size_t(z) * p.nseq + s) * H + k]);
+    x[k] = np_tanhf(__fadd_rn(v, p.pool_b[k]), &tt);
+  }
+  __syncwarp();
   float lg[HEAD_MAX_LABELS];
   for (int l = 0; l < L; ++l) lg[l] = __fadd_rn(warp_dot(x, p.head_wt + size_t(l) * H, H), p.head_b[l]);
-  if (threadIdx.x % 32 == 0) {
+  if (lane == 0) {
     float pr[HEAD_MAX_LABELS];
     int lab;
     softmax_argmax(lg, pr, &lab, L);

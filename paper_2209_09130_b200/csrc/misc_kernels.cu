@@ -4,18 +4,32 @@
 
 namespace samp {
 
-cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st) {
+template <int H>
+static cudaError_t embed_h(const EmbedParams& p, cudaStream_t st) {
   static thread_local int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured != dev) {
-    cudaError_t e = cudaFuncSetAttribute(embed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(embed_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e != cudaSuccess) return e;
     configured = dev;
   }
-  const size_t smem = size_t(EMB_TOK) * (p.hidden + EMB_PAD) * sizeof(float);
-  embed_kernel<<<(p.T + EMB_TOK - 1) / EMB_TOK, EMB_THREADS, smem, st>>>(p);
+  constexpr int tok = EMB_THREADS / 32;
+  embed_kernel<H><<<(p.T + tok - 1) / tok, EMB_THREADS, size_t(tok) * H * sizeof(float), st>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st) {
+  switch (p.hidden) {
+    case 64: return embed_h<64>(p, st);
+    case 128: return embed_h<128>(p, st);
+    case 256: return embed_h<256>(p, st);
+    case 384: return embed_h<384>(p, st);
+    case 512: return embed_h<512>(p, st);
+    case 768: return embed_h<768>(p, st);
+    case 1024: return embed_h<1024>(p, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_classify(const HeadParams& p, cudaStream_t st) {
@@ -27,11 +41,13 @@ cudaError_t launch_classify(const HeadParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = dev;
   }
-  const dim3 grid((p.hidden_size + POOL_COLS - 1) / POOL_COLS, (p.nseq + POOL_SEQS - 1) / POOL_SEQS);
-  pooler_kernel<<<grid, HEAD_THREADS, (size_t(POOL_SEQS) * p.hidden_size + 8 * POOL_SEQS * 32) * sizeof(float), st>>>(p);
+  const dim3 grid((p.hidden_size + POOL_COLS - 1) / POOL_COLS, (p.nseq + POOL_SEQS - 1) / POOL_SEQS, POOL_KSPLIT);
+  const size_t smem = (size_t(POOL_SEQS) * p.hidden_size / POOL_KSPLIT + 8 * POOL_SEQS * 32) * sizeof(float);
+  pooler_kernel<<<grid, HEAD_THREADS, smem, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  classifier_kernel<<<(p.nseq + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32), HEAD_THREADS, 0, st>>>(p);
+  classifier_kernel<<<(p.nseq + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32), HEAD_THREADS,
+                      size_t(HEAD_THREADS / 32) * p.hidden_size * sizeof(float), st>>>(p);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,13 @@ int samp_forward(samp_engine* e, const uint8_t* layer_prec, int32_t nseq, const 
                  const int32_t* att_len, const int32_t* ids, const int32_t* segs, int32_t io,
                  const samp_outputs* out, void* stream);
 
+/* Engine.calibrate (encoder.py:446-454): all-FP forward of the packed batch (host arrays)
+ * with max|x| taps at the 1 + 8L activation sites; amax_out[1 + 8L] in activation_sites
+ * order (embed.out, then per layer attn.in q k v softmax out_in ffn.in ffn.mid).  FP16
+ * tensor-core arithmetic: amax agree with the reference's FP32 calibration to ~1e-3. */
+int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_start, const int32_t* att_len,
+                   const int32_t* ids, const int32_t* segs, double* amax_out);
+
 /* synchronise the engine's stream */
 int samp_sync(samp_engine* e);
 

@@ -45,6 +45,8 @@ struct AttnParams {
   float mult_ctx;             // INT8: F32(s_softmax*s_v)
   float s_ctx;                // INT8: F32(scale(L.attn.out_in))
   int tmem_cols;              // power of two >= max(64, padded keys in the batch)
+  float* amax;                // FP16 calibration: site amax array (null = off)
+  int site_sm, site_ctx;      // L.attn.softmax / L.attn.out_in
 };
 
 template <bool F16>
@@ -257,6 +259,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     const Recip rden = make_recip(denom), rsm = make_recip(F16 ? 1.0f : p.s_softmax);
     // pass 3: P = e / sum (quantized or f16) into the 128B-swizzled K-major A operand
     uint8_t* prow = smem + lay.p_off + r * 128;
+    const bool row_live = q0 + r < S;
+    float amx_sm = 0.0f;
     for (int ch = 0; ch < nchunks; ++ch) {
       if (ch > 0) mbar_wait(bar_pf, (ch - 1) & 1);    // previous round consumed the buffer
       const int k_lo = ch * ATT_P_CHUNK, k_hi = min(nkp, k_lo + ATT_P_CHUNK);
@@ -270,6 +274,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
           for (int j = 0; j < 32; j += 2) {
             const float a = (c0 + j) < S ? div_fast(__uint_as_float(v[j]), rden) : 0.0f;
             const float b = (c0 + j + 1) < S ? div_fast(__uint_as_float(v[j + 1]), rden) : 0.0f;
+            if (row_live) amx_sm = fmaxf(amx_sm, fmaxf(a, b));
             __half2 hv = __floats2half2_rn(a, b);
             w[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
           }
@@ -305,6 +310,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     tmem_ld32(ta + 32 * h, o);
     tmem_wait_ld();
     const Recip rctx = make_recip(F16 ? 1.0f : p.s_ctx);
+    float amx_ctx = 0.0f;
     if (q0 + r < S) {
       if constexpr (F16) {
         __half* dst = static_cast<__half*>(p.ctx_out) + size_t(row0 + q0 + r) * p.hidden + head * 64 + 32 * h;
@@ -317,6 +323,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
         for (int u = 0; u < 4; ++u) d4[u] = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+        if (p.amax) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) amx_ctx = fmaxf(amx_ctx, fabsf(__uint_as_float(o[j])));
+        }
       } else {
         int8_t* dst = static_cast<int8_t*>(p.ctx_out) + size_t(row0 + q0 + r) * p.hidden + head * 64 + 32 * h;
         uint32_t w[8];
@@ -331,6 +341,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
         reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
       }
+    }
+    if (F16 && p.amax) {
+      amax_commit(p.amax + p.site_sm, amx_sm);
+      amax_commit(p.amax + p.site_ctx, amx_ctx);
     }
   }
   tc_fence_before();

@@ -38,6 +38,8 @@ struct EmbedParams {
   __half* out_f16;          // [T][H] or null
   int8_t* out_i8;           // [T][H] or null
   float s_out;              // F32(scale(embed.out)) for out_i8
+  float* amax;              // calibration: amax array (null = off); taps embed.out and L0.attn.in
+  int site, site2;
 };
 
 // numpy pairwise sum of v(i), i in [0, n), evaluated by an 8-lane group (lane j = g)
@@ -163,6 +165,7 @@ static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedPa
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
   const Recip rq = make_recip(p.out_i8 ? p.s_out : 1.0f);
   const size_t base = size_t(t) * H;
+  float amx = 0.0f;
   for (int c = lane * 4; c < H; c += 128) {
     const float4 xv = *reinterpret_cast<const float4*>(row + c);
     const float4 gv = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
@@ -173,6 +176,7 @@ static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedPa
     for (int u = 0; u < 4; ++u) {
       y[u] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xx[u], mean), inv), gg[u]), bb[u]);
       if (p.f16_round) y[u] = __half2float(__float2half_rn(y[u]));
+      amx = fmaxf(amx, fabsf(y[u]));
     }
     if (p.out_f32) *reinterpret_cast<float4*>(p.out_f32 + base + c) = make_float4(y[0], y[1], y[2], y[3]);
     if (p.out_f16) {
@@ -185,6 +189,10 @@ static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedPa
                           ((uint32_t(quant_fast(y[2], rq)) & 0xff) << 16) | (uint32_t(quant_fast(y[3], rq)) << 24);
       *reinterpret_cast<uint32_t*>(p.out_i8 + base + c) = wv;
     }
+  }
+  if (p.amax) {
+    amax_commit(p.amax + p.site, amx);
+    amax_commit(p.amax + p.site2, amx);
   }
 }
 #endif  // SAMP_DEFINE_KERNELS

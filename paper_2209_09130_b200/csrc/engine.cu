@@ -76,7 +76,9 @@ static int pick_bn(int n) {
 static Tiles choose_tiles(int H, int I) {
   Tiles t{};
   t.bn_qkv = pick_bn(H);
-  t.bn_ffn1 = pick_bn(I);
+  // FFN1 (N = I = 4H): 128-wide tiles give 2.6 waves of 2 CTAs/SM at 4096 tokens instead of
+  // 1.3 waves of 256-wide ones (less tail), at the same MMA efficiency
+  t.bn_ffn1 = I % 128 == 0 ? 128 : pick_bn(I);
   const int cand[][2] = {{192, 4}, {256, 4}, {256, 2}, {192, 2}, {256, 1}, {128, 1}, {64, 1}};
   for (auto& c : cand)
     if (c[0] * c[1] == H && pw_splits_evenly(H, c[1])) {
@@ -130,6 +132,7 @@ struct samp_engine {
   std::map<std::string, std::vector<uint8_t>> stages;
   std::vector<int> h_pos;
   bool profiling = false;
+  float* calib_amax = nullptr;    // non-null while samp_calibrate runs: per-site amax taps
   struct Pending { std::string name; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -381,7 +384,9 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
   } else {
     record(e, "in_f32", i, a.hid_f32, size_t(T) * H * 4);
-    EpiF16Out::Params qp{a.qkv_f16, 3 * H, w.qkv_b, 0};
+    float* cal = e->calib_amax;
+    const int cbase = 1 + 8 * i;   // activation_sites order: attn.in q k v softmax out_in ffn.in ffn.mid
+    EpiF16Out::Params qp{a.qkv_f16, 3 * H, w.qkv_b, 0, cal, cbase + 1, H};
     check_launch(e, gemm_f16out(t.bn_qkv, a.a_hid_f16, w.m_qkv_f16, T, 3 * H, 2 * H, qp, st), "qkv_f16");
     AttnParams ap{};
     ap.ctx_out = a.ctx_f16;
@@ -392,6 +397,9 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.hidden = H;
     ap.mult_scores = f32(1.0 / std::sqrt(double(H / e->d.num_heads)));
     ap.tmem_cols = tmem_cols_for_keys(e->geo.max_nkp);
+    ap.amax = cal;
+    ap.site_sm = cbase + 4;
+    ap.site_ctx = cbase + 5;
     launch_attention(e, true, ap);
     EpiResLN::Params lp{};
     lp.bias = w.ob;
@@ -408,6 +416,9 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.out_f32 = a.ln1_f32;
       lp.out_f16 = a.ln1_f16;
       lp.f16_round = fp16_store;
+      lp.amax = cal;
+      lp.site = cbase + 6;
+      lp.site2 = -1;
     }
     check_launch(e, gemm_ln_f16(t, a.a_ctx_f16, w.m_wo_f16, T, H, 2 * H, lp, st), "outproj_f16");
     if (p == SAMP_LAYER_FFN_INT8) record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
@@ -438,11 +449,16 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.mult = mult_of(s_mid, w.s_w[5]);
     check_launch(e, gemm_ln_i8(t, a.a_mid_i8, w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
   } else {
-    EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1};
+    EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
     check_launch(e, gemm_f16out(t.bn_ffn1, a.a_ln1_f16, w.m_w1_f16, T, I, 2 * H, gp, st), "ffn1_f16");
     lp.res_f32 = a.ln1_f32;
     lp.acc_is_f32 = 1;
     lp.f16_round = (p == SAMP_LAYER_FP) ? fp16_store : 0;
+    if (e->calib_amax && i + 1 < L) {   // tap L{i+1}.attn.in
+      lp.amax = e->calib_amax;
+      lp.site = 1 + 8 * (i + 1);
+      lp.site2 = -1;
+    }
     check_launch(e, gemm_ln_f16(t, a.a_mid_f16, w.m_w2_f16, T, H, 2 * I, lp, st), "ffn2_f16");
   }
   if (next_int8) {
@@ -643,6 +659,34 @@ extern "C" int samp_fetch_stage(samp_engine* e, const char* name, int layer, voi
   });
 }
 
+// Engine.calibrate (reference encoder.py:446-454): FP forward (FP16 tensor-core path)
+// with max|x| taps at all 1 + 8L activation sites, in activation_sites order.
+extern "C" int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_start, const int32_t* att_len,
+                              const int32_t* ids, const int32_t* segs, double* amax_out) {
+  int rc = SAMP_OK;
+  rc = guarded([&] {
+    const int n = 1 + 8 * e->d.num_layers;
+    SAMP_CUDA(cudaSetDevice(e->device));
+    float* dev = e->mem.alloc<float>(n);
+    SAMP_CUDA(cudaMemset(dev, 0, n * sizeof(float)));
+    e->calib_amax = dev;
+    std::vector<uint8_t> fp(e->d.num_layers, SAMP_LAYER_FP);
+    samp_outputs none{};
+    const int r = samp_forward(e, fp.data(), nseq, seq_start, att_len, ids, segs, SAMP_IO_HOST, &none, nullptr);
+    e->calib_amax = nullptr;
+    if (r != SAMP_OK) {
+      e->mem.release(dev);
+      throw SampError(r, samp_last_error());
+    }
+    std::vector<float> h(n);
+    SAMP_CUDA(cudaMemcpy(h.data(), dev, n * sizeof(float), cudaMemcpyDeviceToHost));
+    e->mem.release(dev);
+    for (int k = 0; k < n; ++k) amax_out[k] = double(h[k]);
+  });
+  e->calib_amax = nullptr;
+  return rc;
+}
+
 extern "C" int samp_sync(samp_engine* e) {
   return guarded([&] { SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use)); });
 }
@@ -772,6 +816,9 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       ep.out_i8 = a.xq[0];
       ep.s_out = f32(sc(e, "embed.out"));
     }
+    ep.amax = e->calib_amax;   // taps embed.out and L0.attn.in (same tensor)
+    ep.site = 0;
+    ep.site2 = 1;
     check_launch(e, launch_embed(ep, st), "embed");
     record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
     int cur = 0;

@@ -339,6 +339,9 @@ struct EpiF16Out {
     int ldo;
     const float* bias;
     int gelu;
+    float* amax;          // calibration: site amax array (null = off)
+    int site0;            // site of column block 0
+    int block_cols;       // columns per site (QKV: H -> q|k|v sites); 0 = one site
   };
   template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
@@ -351,6 +354,7 @@ struct EpiF16Out {
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
     const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
     const float* sbias = reinterpret_cast<const float*>(smem + sizeof(TanhTable));
+    float amx = 0.0f;
 #pragma unroll 1
     for (int col = 0; col < c.ncols; col += 32) {
       const int gcol = c.n0 + c.c0 + col;
@@ -368,6 +372,7 @@ struct EpiF16Out {
           x0 = gelu_ref(x0, tt);
           x1 = gelu_ref(x1, tt);
         }
+        if (c.row < c.M) amx = fmaxf(amx, fmaxf(fabsf(x0), fabsf(x1)));
         __half2 h = __floats2half2_rn(x0, x1);
         packed[j / 2] = *reinterpret_cast<uint32_t*>(&h);
       }
@@ -377,6 +382,7 @@ struct EpiF16Out {
         for (int j = 0; j < 4; ++j) dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
       }
     }
+    if (p.amax) amax_commit(p.amax + p.site0 + (p.block_cols ? c.n0 / p.block_cols : 0), amx);
   }
 };
 
@@ -404,6 +410,8 @@ struct EpiResLN {
     int f16_round;                  // reference fp16 storage: round the f32 output through f16
     float* out_f32;                 // optional
     __half* out_f16;                // optional
+    float* amax;                    // calibration: amax array (null = off)
+    int site, site2;                // sites tapped with the emitted values (site2 < 0: none)
   };
   // smem: [0,512) floats reduction scratch (per-half partials, 2 x CTA partials), then
   // bias / gamma / beta slices (BN floats each), then the int8 residual tile
@@ -542,6 +550,7 @@ struct EpiResLN {
     const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
     const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);
+    float amx = 0.0f;
 
     // pass 3: normalise, affine, emit
 #pragma unroll 1
@@ -572,6 +581,10 @@ struct EpiResLN {
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
       }
+      if (p.amax) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) amx = fmaxf(amx, fabsf(y[j]));
+      }
       if (p.out_f32) {
         float4* dst = reinterpret_cast<float4*>(p.out_f32 + rbase + gcol);
 #pragma unroll
@@ -587,6 +600,10 @@ struct EpiResLN {
                               *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
         }
       }
+    }
+    if (p.amax) {
+      amax_commit(p.amax + p.site, amx);
+      if (p.site2 >= 0) amax_commit(p.amax + p.site2, amx);
     }
   }
 };

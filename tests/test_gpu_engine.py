@@ -213,3 +213,49 @@ def test_errors_raised_before_compute(bert2):
             eng.run(EncodedInput([1, 2], [0, 0], 2), plan)
     finally:
         arch.calibration = saved
+
+
+def test_gpu_calibration_matches_reference_semantics(bert2):
+    """Engine.calibrate on the device (FP16 path + amax taps) vs the reference-style FP32
+    calibration computed by the oracle on the same inputs."""
+    arch, _ = bert2
+    eng = _engine(arch)
+    rng = np.random.default_rng(3)
+    seqs = [rng.integers(4, 1000, 64).tolist() for _ in range(2)]     # the fixture's inputs
+    table = eng.calibrate([EncodedInput(s, [0] * len(s), len(s)) for s in seqs])
+    ref = _calibrate_with_oracle(_bert_like(), seqs)
+    assert set(table.entries) == set(ref)
+    worst = max(abs(table.amax(s) - a) / a for s, a in ref.items())
+    print(f"max relative amax deviation {worst:.2e}")
+    assert worst < 2e-2
+
+
+def test_mha_only_extension_matches_composed_oracle(bert2):
+    arch, amax = bert2
+    eng = _engine(arch)
+    model = orc.Model.from_manifest(arch.manifest, arch.tensors, amax)
+    rng = np.random.default_rng(13)
+    for enc in _batch(rng, [(64, 64), (80, 60)]):
+        for k in (1, 2):
+            plan = PrecisionPlan.prefix("MHA_ONLY", 2, k)
+            got = eng.run(enc, plan).hidden_states
+            want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
+            _fp16_close(got, want, f"MHA_ONLY k={k}")
+
+
+def test_trace_and_sweep_on_device(bert2):
+    from paper_2209_09130_b200 import allocator as al
+    from paper_2209_09130_b200.trace import trace_ops
+    arch, _ = bert2
+    eng = _engine(arch)
+    enc = EncodedInput(list(range(4, 68)), [0] * 64, 64)
+    with trace_ops() as tr:
+        eng.run(enc, PrecisionPlan.prefix("FULLY_QUANT", 2, 2))
+    assert tr.gemm_count("i8") == 12 and tr.gemm_count("f32") == 0
+    examples = [(" ".join(f"w{j}" for j in range(i, i + 20)), None, str(i % 2)) for i in range(6)]
+    prof = al.build_profile(eng, "FULLY_QUANT", examples, layer_step=1, repeats=3, warmup=1)
+    assert [p.quantized_layers for p in prof.points] == [0, 1, 2]
+    assert prof.env["gemm_stats"]["2"]["int8_gemms"] == 12
+    assert all(p.latency > 0 for p in prof.points)
+    idx = al.allocate_decay_aware(prof)
+    assert 0 <= idx < len(prof.points)

@@ -108,6 +108,10 @@ int samp_forward(samp_engine* e, const uint8_t* layer_prec, int32_t nseq, const 
 int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_start, const int32_t* att_len,
                    const int32_t* ids, const int32_t* segs, double* amax_out);
 
+/* CUDA-graph replay of the forward per (plan, batch geometry, head): on by default;
+ * a key is captured on its second use and replayed afterwards */
+int samp_set_graphs(samp_engine* e, int on);
+
 /* synchronise the engine's stream */
 int samp_sync(samp_engine* e);
 

@@ -133,6 +133,13 @@ struct samp_engine {
   std::vector<int> h_pos;
   bool profiling = false;
   float* calib_amax = nullptr;    // non-null while samp_calibrate runs: per-site amax taps
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    int launches;
+  };
+  bool graphs_enabled = true;
+  std::map<std::string, GraphEntry> graphs;   // (plan, geometry, head) -> captured forward
+  std::set<std::string> seen;
   struct Pending { std::string name; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -143,9 +150,20 @@ struct samp_engine {
 
 namespace samp {
 
+using GraphEntry = samp_engine::GraphEntry;
+
+// captured graphs bake buffer pointers, tensor maps and scales: drop them whenever any changes
+static void clear_graphs(samp_engine* e) {
+  for (auto& kv : e->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  e->graphs.clear();
+  e->seen.clear();
+}
+
 static void ensure_activations(samp_engine* e, int T) {
   Activations& a = e->act;
   if (T <= a.cap) return;
+  clear_graphs(e);
   int cap = std::max(T, 256);
   cap = (cap + 127) / 128 * 128;
   const int H = e->d.hidden, I = e->d.intermediate, L = std::max(1, e->d.num_labels);
@@ -469,6 +487,62 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   }
 }
 
+
+// embed -> layers -> head for the current geometry, all launched on `st`
+static void enqueue_kernels(samp_engine* e, const uint8_t* prec, int nseq, int head, cudaStream_t st) {
+  // ---------------- embedding (+ quantize at embed.out when layer 0 is INT8-attention)
+  const samp_model_desc& d = e->d;
+  const int L = d.num_layers, H = d.hidden, T = e->geo.T;
+  Activations& a = e->act;
+  const bool first_int8 = prec[0] == SAMP_LAYER_FULL_INT8 || prec[0] == SAMP_LAYER_MHA_INT8;
+  EmbedParams ep{};
+  ep.ids = a.ids;
+  ep.segs = a.segs;
+  ep.pos = a.pos;
+  ep.word = e->word;
+  ep.position = e->position;
+  ep.token_type = e->token_type;
+  ep.gamma = e->emb_g;
+  ep.beta = e->emb_b;
+  ep.eps = f32(d.layernorm_eps);
+  ep.hidden = H;
+  ep.T = T;
+  ep.f16_round = d.fp16_storage;
+  ep.out_f32 = a.hid_f32;
+  ep.out_f16 = a.hid_f16;
+  if (first_int8) {
+    ep.out_i8 = a.xq[0];
+    ep.s_out = f32(sc(e, "embed.out"));
+  }
+  ep.amax = e->calib_amax;   // taps embed.out and L0.attn.in (same tensor)
+  ep.site = 0;
+  ep.site2 = 1;
+  check_launch(e, launch_embed(ep, st), "embed");
+  record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
+  int cur = 0;
+  for (int i = 0; i < L; ++i) run_layer(e, i, prec, cur);
+  // ---------------- heads + outputs (final hidden is always F32 in hid_f32)
+  const int nl = d.num_labels;
+  if (head != SAMP_HEAD_NONE) {
+    HeadParams hp{};
+    hp.hidden = a.hid_f32;
+    hp.seq_start = e->geo.d_seq_start;
+    hp.pool_w = e->pool_w;
+    hp.pooled = a.pooled;
+    hp.pool_b = e->pool_b;
+    hp.head_wt = e->head_wt;
+    hp.head_b = e->head_b;
+    hp.hidden_size = H;
+    hp.num_labels = nl;
+    hp.nseq = nseq;
+    hp.T = T;
+    hp.logits = a.logits;
+    hp.probs = a.probs;
+    hp.labels = a.labels;
+    check_launch(e, head == SAMP_HEAD_CLASSIFY ? launch_classify(hp, st) : launch_tag(hp, st), "head");
+  }
+}
+
 }  // namespace samp
 
 using namespace samp;
@@ -511,6 +585,7 @@ extern "C" void samp_engine_destroy(samp_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   cudaDeviceSynchronize();
+  clear_graphs(e);
   if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
   cudaStreamDestroy(e->stream);
   delete e;
@@ -631,11 +706,24 @@ extern "C" int samp_weight_scales(samp_engine* e, int layer, double* out6) {
 }
 
 extern "C" int samp_set_site_amax(samp_engine* e, const char* site, double amax) {
-  return guarded([&] { e->amax[site] = amax; });
+  return guarded([&] {
+    clear_graphs(e);
+    e->amax[site] = amax;
+  });
 }
 
 extern "C" int samp_clear_calibration(samp_engine* e) {
-  return guarded([&] { e->amax.clear(); });
+  return guarded([&] {
+    clear_graphs(e);
+    e->amax.clear();
+  });
+}
+
+extern "C" int samp_set_graphs(samp_engine* e, int on) {
+  return guarded([&] {
+    clear_graphs(e);
+    e->graphs_enabled = on != 0;
+  });
 }
 
 extern "C" int samp_set_capture(samp_engine* e, int on) {
@@ -795,54 +883,43 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       SAMP_CUDA(cudaMemcpyAsync(a.ids, ids, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
       SAMP_CUDA(cudaMemcpyAsync(a.segs, segs, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
     }
-    // ---------------- embedding (+ quantize at embed.out when layer 0 is INT8-attention)
-    const bool first_int8 = prec[0] == SAMP_LAYER_FULL_INT8 || prec[0] == SAMP_LAYER_MHA_INT8;
-    EmbedParams ep{};
-    ep.ids = a.ids;
-    ep.segs = a.segs;
-    ep.pos = a.pos;
-    ep.word = e->word;
-    ep.position = e->position;
-    ep.token_type = e->token_type;
-    ep.gamma = e->emb_g;
-    ep.beta = e->emb_b;
-    ep.eps = f32(d.layernorm_eps);
-    ep.hidden = H;
-    ep.T = T;
-    ep.f16_round = d.fp16_storage;
-    ep.out_f32 = a.hid_f32;
-    ep.out_f16 = a.hid_f16;
-    if (first_int8) {
-      ep.out_i8 = a.xq[0];
-      ep.s_out = f32(sc(e, "embed.out"));
+    // ---------------- device work: replay a captured CUDA graph for this (plan, batch
+    // geometry, head) when one exists; capture on the second sighting of a key (the first
+    // run also configures every kernel's smem attributes outside of capture)
+    const bool graphable = e->graphs_enabled && !e->capture && !e->profiling && !e->calib_amax;
+    std::string key;
+    if (graphable) {
+      key.assign(reinterpret_cast<const char*>(prec), L);
+      key += char(head);
+      key.append(reinterpret_cast<const char*>(seq_start), (nseq + 1) * sizeof(int32_t));
+      key.append(reinterpret_cast<const char*>(att_len), nseq * sizeof(int32_t));
     }
-    ep.amax = e->calib_amax;   // taps embed.out and L0.attn.in (same tensor)
-    ep.site = 0;
-    ep.site2 = 1;
-    check_launch(e, launch_embed(ep, st), "embed");
-    record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
-    int cur = 0;
-    for (int i = 0; i < L; ++i) run_layer(e, i, prec, cur);
-    // ---------------- heads + outputs (final hidden is always F32 in hid_f32)
+    auto it = graphable ? e->graphs.find(key) : e->graphs.end();
+    if (it != e->graphs.end() && it->second.exec) {
+      SAMP_CUDA(cudaGraphLaunch(it->second.exec, st));
+      e->launches = it->second.launches;
+    } else if (graphable && e->seen.count(key)) {
+      if (e->graphs.size() >= 64) clear_graphs(e);
+      cudaGraph_t g = nullptr;
+      SAMP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_kernels(e, prec, nseq, head, st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      SAMP_CUDA(cudaStreamEndCapture(st, &g));
+      cudaGraphExec_t exec = nullptr;
+      SAMP_CUDA(cudaGraphInstantiate(&exec, g, 0));
+      cudaGraphDestroy(g);
+      e->graphs[key] = GraphEntry{exec, e->launches};
+      SAMP_CUDA(cudaGraphLaunch(exec, st));
+    } else {
+      enqueue_kernels(e, prec, nseq, head, st);
+      if (graphable) e->seen.insert(key);
+    }
     const int nl = d.num_labels;
-    if (head != SAMP_HEAD_NONE) {
-      HeadParams hp{};
-      hp.hidden = a.hid_f32;
-      hp.seq_start = e->geo.d_seq_start;
-      hp.pool_w = e->pool_w;
-      hp.pooled = a.pooled;
-      hp.pool_b = e->pool_b;
-      hp.head_wt = e->head_wt;
-      hp.head_b = e->head_b;
-      hp.hidden_size = H;
-      hp.num_labels = nl;
-      hp.nseq = nseq;
-      hp.T = T;
-      hp.logits = a.logits;
-      hp.probs = a.probs;
-      hp.labels = a.labels;
-      check_launch(e, head == SAMP_HEAD_CLASSIFY ? launch_classify(hp, st) : launch_tag(hp, st), "head");
-    }
     const cudaMemcpyKind kind = io == SAMP_IO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (out) {
       if (out->hidden) SAMP_CUDA(cudaMemcpyAsync(out->hidden, a.hid_f32, size_t(T) * H * 4, kind, st));

@@ -259,3 +259,18 @@ def test_trace_and_sweep_on_device(bert2):
     assert all(p.latency > 0 for p in prof.points)
     idx = al.allocate_decay_aware(prof)
     assert 0 <= idx < len(prof.points)
+
+
+def test_cuda_graph_replay_is_bit_identical(bert2):
+    arch, _ = bert2
+    eng = _engine(arch)
+    rng = np.random.default_rng(21)
+    encs = _batch(rng, [(128, 128), (64, 40)])
+    plan = PrecisionPlan.prefix("FULLY_QUANT", 2, 2)
+    outs = [eng.run_batch(encs, plan) for _ in range(4)]       # run, capture, replay, replay
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o.hidden_states, outs[0].hidden_states)
+        np.testing.assert_array_equal(o.logits, outs[0].logits)
+    # geometry change invalidates nothing incorrectly
+    other = eng.run_batch(encs[:1], plan)
+    np.testing.assert_array_equal(other.sequence(0), outs[0].sequence(0))

@@ -463,8 +463,151 @@ struct EpiResLN {
     return s;
   }
 
+  // residual of 32 columns starting at tile column `col` (int8 tile in smem, or f32 global)
+  template <int BN>
+  __device__ static void residual32(const Params& p, const EpiCtx& c, const uint8_t* rtile, size_t rbase,
+                                    int col, float (&res)[32]) {
+    if (p.res_i8) {
+      const uint4* src = reinterpret_cast<const uint4*>(rtile + col);
+      const uint4 u0 = src[0], u1 = src[1];
+      const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+      for (int j = 0; j < 32; ++j) res[j] = deq(int(int8_t((w[j / 4] >> (8 * (j % 4))) & 0xff)), p.res_scale);
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(p.res_f32 + rbase + c.n0 + col);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = src[j];
+        res[4 * j] = v.x; res[4 * j + 1] = v.y; res[4 * j + 2] = v.z; res[4 * j + 3] = v.w;
+      }
+    }
+  }
+
+  // emit 32 normalised values (quantize / deq / f16 round / amax / stores)
+  __device__ static void emit32(const Params& p, size_t rbase, int gcol, const Recip& rq, float (&y)[32], float& amx) {
+    if (p.out_i8 || p.deq_outputs) {
+      int q[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) q[j] = quant_fast(y[j], rq);
+      if (p.out_i8) store32_i8(p.out_i8 + rbase + gcol, q);
+      if (p.deq_outputs) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
+      }
+    }
+    if (p.f16_round) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
+    }
+    if (p.amax) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) amx = fmaxf(amx, fabsf(y[j]));
+    }
+    if (p.out_f32) {
+      float4* dst = reinterpret_cast<float4*>(p.out_f32 + rbase + gcol);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dst[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+    }
+    if (p.out_f16) {
+      uint4* dst = reinterpret_cast<uint4*>(p.out_f16 + rbase + gcol);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __half2 h0 = __floats2half2_rn(y[8 * j], y[8 * j + 1]), h1 = __floats2half2_rn(y[8 * j + 2], y[8 * j + 3]);
+        __half2 h2 = __floats2half2_rn(y[8 * j + 4], y[8 * j + 5]), h3 = __floats2half2_rn(y[8 * j + 6], y[8 * j + 7]);
+        dst[j] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                            *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+      }
+    }
+  }
+
+  // Register-resident variant (1 CTA/SM tiles, NE == 8): the thread's whole (half) row is
+  // pulled out of TMEM once; sums, normalisation and outputs all run from registers.
+  template <int BN, int CLUSTER, int NE>
+  __device__ static void run_regs(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    constexpr int NC = BN / (NE / 4);
+    static_assert(NC % 32 == 0 && NC <= 128, "one numpy leaf per thread");
+    float* halves = reinterpret_cast<float*>(smem);
+    float* cta0 = halves + 256;
+    float* cta1 = cta0 + 128;
+    const float* sbias = halves + RED_FLOATS;
+    const float* sgam = sbias + BN;
+    const float* sbet = sgam + BN;
+    const uint8_t* rtile = smem + (RED_FLOATS + 3 * BN) * 4 + c.tile_row * res_ld<BN>();
+    const bool valid = c.row < c.M;
+    const size_t rbase = size_t(valid ? c.row : 0) * p.hidden;
+    float x[NC];
+    {
+      uint32_t r[NC];
+#pragma unroll
+      for (int k = 0; k < NC / 32; ++k)
+        tmem_ld32(c.taddr + 32 * k, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * k));
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < NC / 32; ++k) {
+        float res[32];
+        residual32<BN>(p, c, rtile, rbase, c.c0 + 32 * k, res);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t u = r[32 * k + j];
+          const float acc = p.acc_is_f32 ? __uint_as_float(u) : __fmul_rn(__int2float_rn(int(u)), p.mult);
+          x[32 * k + j] = __fadd_rn(__fadd_rn(acc, sbias[c.c0 + 32 * k + j]), res[j]);
+        }
+      }
+    }
+    // one numpy leaf of NC elements: 8 strided accumulators, then ((0+1)+(2+3))+((4+5)+(6+7))
+    auto leaf = [&](auto f) {
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = f(x[j]);
+#pragma unroll
+      for (int g = 1; g < NC / 8; ++g)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], f(x[8 * g + j]));
+      return __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                       __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+    };
+    const float hf = float(p.hidden);
+    const float total = reduce_row<CLUSTER, NE>(leaf([](float v) { return v; }), c, halves, cta0);
+    const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
+    const float total2 = reduce_row<CLUSTER, NE>(leaf([mean](float v) {
+                                                   const float d = __fsub_rn(v, mean);
+                                                   return __fmul_rn(d, d);
+                                                 }),
+                                                 c, halves, cta1);
+    const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+    const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);
+    float amx = 0.0f;
+    if (valid) {
+#pragma unroll
+      for (int k = 0; k < NC / 32; ++k) {
+        float y[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = c.c0 + 32 * k + j;
+          y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[32 * k + j], mean), inv), sgam[col]), sbet[col]);
+        }
+        emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+      }
+    }
+    if (p.amax) {
+      amax_commit(p.amax + p.site, amx);
+      if (p.site2 >= 0) amax_commit(p.amax + p.site2, amx);
+    }
+  }
+
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    if constexpr (NE == 8 && (BN / 2) % 32 == 0 && BN / 2 <= 128) {
+      run_regs<BN, CLUSTER, NE>(p, c, smem);
+    } else {
+      run_tmem<BN, CLUSTER, NE>(p, c, smem);
+    }
+  }
+
+  // TMEM-resident variant (generic shapes)
+  template <int BN, int CLUSTER, int NE>
+  __device__ static void run_tmem(const Params& p, const EpiCtx& c, uint8_t* smem) {
     float* halves = reinterpret_cast<float*>(smem);
     float* cta0 = halves + 256;
     float* cta1 = cta0 + 128;

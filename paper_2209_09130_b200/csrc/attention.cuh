@@ -177,18 +177,30 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     tc_fence_after();
 
     // pass 1: x = acc*mult + mask -> TMEM, row max over the S real keys
+    // (chunks entirely inside [0, min(att, S)) skip the per-key mask / bounds checks)
     float mx = -INFINITY;
+    const int clean = min(att, S);
     for (int c0 = 32 * h; c0 < nkp; c0 += 64) {
       uint32_t v[32];
       tmem_ld32(ta + c0, v);
       tmem_wait_ld();
+      if (c0 + 32 <= clean) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int key = c0 + j;
-        const float acc = F16 ? __uint_as_float(v[j]) : __int2float_rn(int(v[j]));
-        const float x = __fadd_rn(__fmul_rn(acc, p.mult_scores), key < att ? 0.0f : -10000.0f);
-        if (key < S) mx = fmaxf(mx, x);
-        v[j] = __float_as_uint(x);
+        for (int j = 0; j < 32; ++j) {
+          const float acc = F16 ? __uint_as_float(v[j]) : __int2float_rn(int(v[j]));
+          const float x = __fadd_rn(__fmul_rn(acc, p.mult_scores), 0.0f);
+          mx = fmaxf(mx, x);
+          v[j] = __float_as_uint(x);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int key = c0 + j;
+          const float acc = F16 ? __uint_as_float(v[j]) : __int2float_rn(int(v[j]));
+          const float x = __fadd_rn(__fmul_rn(acc, p.mult_scores), key < att ? 0.0f : -10000.0f);
+          if (key < S) mx = fmaxf(mx, x);
+          v[j] = __float_as_uint(x);
+        }
       }
       tmem_st32(ta + c0, v);
     }
@@ -196,15 +208,20 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     xch[h * 128 + r] = mx;
     att_bar();
     mx = fmaxf(xch[r], xch[128 + r]);
-    // pass 2: e = exp(x - max) -> TMEM (0 past S)
+    // pass 2: e = exp(x - max) -> TMEM (0 past S); x - max <= 0 (numpy exp on that domain)
     for (int c0 = 32 * h; c0 < nkp; c0 += 64) {
       uint32_t v[32];
       tmem_ld32(ta + c0, v);
       tmem_wait_ld();
+      if (c0 + 32 <= S) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float e = (c0 + j) < S ? np_expf(__fsub_rn(__uint_as_float(v[j]), mx)) : 0.0f;
-        v[j] = __float_as_uint(e);
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(np_expf_nonpos(__fsub_rn(__uint_as_float(v[j]), mx)));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float e = (c0 + j) < S ? np_expf_nonpos(__fsub_rn(__uint_as_float(v[j]), mx)) : 0.0f;
+          v[j] = __float_as_uint(e);
+        }
       }
       tmem_st32(ta + c0, v);
     }
@@ -284,7 +301,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
             int q[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              q[u] = (c0 + j + u) < S ? quant_fast(div_fast(__uint_as_float(v[j + u]), rden), rsm) : 0;
+              q[u] = (c0 + j + u) < S ? quant_bounded(div_fast(__uint_as_float(v[j + u]), rden), rsm) : 0;
             w[j / 4] = (uint32_t(q[0]) & 0xff) | ((uint32_t(q[1]) & 0xff) << 8) |
                        ((uint32_t(q[2]) & 0xff) << 16) | ((uint32_t(q[3]) & 0xff) << 24);
           }
@@ -334,7 +351,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         for (int j = 0; j < 32; j += 4) {
           int q[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) q[u] = quant_fast(__fmul_rn(__int2float_rn(int(o[j + u])), p.mult_ctx), rctx);
+          for (int u = 0; u < 4; ++u) q[u] = quant_bounded(__fmul_rn(__int2float_rn(int(o[j + u])), p.mult_ctx), rctx);
           w[j / 4] = (uint32_t(q[0]) & 0xff) | ((uint32_t(q[1]) & 0xff) << 8) |
                      ((uint32_t(q[2]) & 0xff) << 16) | ((uint32_t(q[3]) & 0xff) << 24);
         }

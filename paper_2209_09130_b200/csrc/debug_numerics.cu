@@ -34,7 +34,9 @@ __global__ void quant_exhaustive_kernel(const float* scales, int n, unsigned lon
          u += uint64_t(gridDim.x) * blockDim.x) {
       const float x = __uint_as_float(uint32_t(u));
       if (x != x) continue;  // NaN codes are unspecified in the reference (clip keeps NaN)
-      local += quant_fast(x, r) != quant_i8(x, s);
+      const int want = quant_i8(x, s);
+      local += quant_fast(x, r) != want;
+      if (fabsf(x) < 1.1529215e18f) local += quant_bounded(x, r) != want;   // |x| < 2^60
     }
   }
   atomicAdd(bad, local);
@@ -65,6 +67,7 @@ __global__ void exp_exhaustive_kernel(unsigned long long* bad) {
     const float x = __uint_as_float(uint32_t(u));
     const float a = np_expf(x), b = np_expf_ieee(x);
     local += (__float_as_uint(a) != __float_as_uint(b)) && !(a != a && b != b);
+    if (x <= 0.0f) local += __float_as_uint(np_expf_nonpos(x)) != __float_as_uint(b);
   }
   atomicAdd(bad, local);
 }

@@ -275,7 +275,7 @@ struct EpiQKV {
       int q[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        q[j] = quant_fast(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j])), mult), b[j]), rq);
+        q[j] = quant_bounded(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j])), mult), b[j]), rq);
       if (c.row < c.M) store32_i8(p.out + size_t(c.row) * p.ldo + gcol, q);
     }
   }
@@ -323,8 +323,8 @@ struct EpiGeluQuant {
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
         gelu8(v, tt);
-        w[g / 4] = pack4_i8(quant_fast(v[0], rq), quant_fast(v[1], rq), quant_fast(v[2], rq), quant_fast(v[3], rq));
-        w[g / 4 + 1] = pack4_i8(quant_fast(v[4], rq), quant_fast(v[5], rq), quant_fast(v[6], rq), quant_fast(v[7], rq));
+        w[g / 4] = pack4_i8(quant_bounded(v[0], rq), quant_bounded(v[1], rq), quant_bounded(v[2], rq), quant_bounded(v[3], rq));
+        w[g / 4 + 1] = pack4_i8(quant_bounded(v[4], rq), quant_bounded(v[5], rq), quant_bounded(v[6], rq), quant_bounded(v[7], rq));
       }
       if (c.row < c.M) *reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol) = make_uint4(w[0], w[1], w[2], w[3]);
     }

@@ -140,6 +140,13 @@ int samp_last_launch_count(samp_engine* e);
 /* per-kernel device timing: with profiling on, every launch is bracketed by CUDA events
  * on the engine stream; samp_profile_report syncs and writes {"kernel": [total_ms, n], ...} */
 int samp_set_profiling(samp_engine* e, int on);
+/* GEMM phase stamps (profiling mode only): samp_debug_gemm_stamps(e, n) records, for the
+ * next n GEMM launches, per CTA 8 u64 = {smid, t_start, t_first_slot_full, t_last_slot_full,
+ * t_accumulator_done, t_epilogue_done, t_exit, 0} (%globaltimer ns), 1024 CTAs per launch;
+ * _fetch copies them out with the launch names ('\n'-separated) and resets the list. */
+int samp_debug_gemm_stamps(samp_engine* e, int max_launches);
+int samp_debug_gemm_stamps_fetch(samp_engine* e, unsigned long long* out, int cap_launches, char* names,
+                                 size_t names_cap, int* n_launches);
 int samp_profile_report(samp_engine* e, char* buf, size_t cap);
 
 #ifdef __cplusplus

@@ -38,20 +38,23 @@ def _stale(obj: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB, objdir: str = OBJDIR) -> str:
+    """Compile every csrc/*.cu for sm_100a and link `lib`.  `defines` (e.g. ["SAMP_X=1"])
+    and a separate `objdir`/`lib` build measurement variants next to the product library."""
+    os.makedirs(objdir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     jobs = []
     for src in sources:
-        obj = os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         if force or _stale(obj, [src] + headers):
             jobs.append((src, obj))
 
     def compile_one(job):
         src, obj = job
-        cmd = [nvcc()] + ARCH + NVCC_FLAGS + ["-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
+        cmd = [nvcc()] + ARCH + NVCC_FLAGS + ["-D" + d for d in defines] + ["-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {os.path.basename(src)}:\n{r.stderr[-6000:]}")
@@ -61,11 +64,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for log in pool.map(compile_one, jobs):
             if verbose and log:
                 print(log)
-    objs = [os.path.join(OBJDIR, os.path.basename(s)[:-3] + ".o") for s in sources]
-    if jobs or not os.path.exists(LIB):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in sources]
+    if jobs or not os.path.exists(lib):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
         subprocess.run(cmd, check=True, capture_output=not verbose)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

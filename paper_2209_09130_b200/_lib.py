@@ -13,7 +13,8 @@ import os
 from . import errors
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libsamp_b200.so")
+# SAMP_B200_LIB: load another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("SAMP_B200_LIB") or os.path.join(_PKG, "lib", "libsamp_b200.so")
 
 SAMP_OK = 0
 _STATUS = {
@@ -75,6 +76,9 @@ SIGNATURES = [
     ("samp_last_launch_count", ctypes.c_int, [ctypes.c_void_p]),
     ("samp_set_profiling", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("samp_profile_report", ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
+    ("samp_debug_gemm_stamps", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    ("samp_debug_gemm_stamps_fetch", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                                     ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p]),
 ]
 
 _lib = None

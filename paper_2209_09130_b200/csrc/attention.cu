@@ -14,8 +14,8 @@ static cudaError_t launch_att(const CUtensorMap& map, const AttnParams& p, int n
     if (e != cudaSuccess) return e;
     configured = dev;
   }
-  attention_kernel<F16><<<dim3(ntiles, heads), ATT_THREADS, AttnLayout<F16>(keys_cap).total, st>>>(map, p, keys_cap);
-  return cudaGetLastError();
+  return launch_ex(attention_kernel<F16>, dim3(ntiles, heads), dim3(ATT_THREADS), AttnLayout<F16>(keys_cap).total,
+                   st, 1, map, p, keys_cap);
 }
 
 cudaError_t launch_attention_i8(const CUtensorMap& map, const AttnParams& p, int ntiles, int heads, int keys_cap,

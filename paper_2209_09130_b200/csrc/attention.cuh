@@ -115,9 +115,9 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr int KIND = F16 ? KIND_F16 : KIND_I8;
-
   if (warp == 0) {
     if (elect_one()) {
+      pdl_wait();   // Q/K/V come from the QKV GEMM; every later access is ordered after this
       const int nblk = (nkp + 63) / 64;
       mbar_expect_tx(bar_load, 128 * C::ROW_BYTES + 2 * nblk * 64 * C::ROW_BYTES);
       const int H = p.hidden;
@@ -160,6 +160,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         }
         mma_commit(bar_pf);
       }
+      pdl_trigger();   // last MMA issued: the next kernel's prologue overlaps our epilogue
     }
     __syncwarp();
   } else {

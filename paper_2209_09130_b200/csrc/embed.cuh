@@ -135,6 +135,8 @@ __device__ __forceinline__ float pairwise_warp(V& v) {
 template <int H>
 static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedParams p) {
   extern __shared__ float xs[];              // [8 warps][H]
+  pdl_trigger();
+  pdl_wait();                                 // xq / hidden buffers are still read by the previous forward
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * (EMB_THREADS / 32) + warp;
   if (t >= p.T) return;                       // warp-uniform

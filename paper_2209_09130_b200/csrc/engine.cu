@@ -132,6 +132,10 @@ struct samp_engine {
   std::map<std::string, std::vector<uint8_t>> stages;
   std::vector<int> h_pos;
   bool profiling = false;
+  // GEMM phase stamps (profiling mode): [stamp_cap launches][STAMP_CTAS][GEMM_STAMPS]
+  unsigned long long* stamps = nullptr;
+  int stamp_cap = 0;
+  std::vector<std::pair<std::string, int>> stamp_launches;   // (name, CTAs) per GEMM launch
   float* calib_amax = nullptr;    // non-null while samp_calibrate runs: per-site amax taps
   struct GraphEntry {
     cudaGraphExec_t exec;
@@ -301,6 +305,8 @@ static cudaEvent_t take_event(samp_engine* e) {
   return ev;
 }
 
+constexpr int STAMP_CTAS = GEMM_STAMP_CTAS;   // CTAs recorded per stamped GEMM launch
+
 // launch through `fn` (returns cudaError_t); with profiling on, bracket it with CUDA
 // events on the engine stream (the stream every kernel is launched on)
 template <class F>
@@ -311,7 +317,16 @@ static void run_kernel(samp_engine* e, const char* what, F&& fn) {
     b = take_event(e);
     SAMP_CUDA(cudaEventRecord(a, e->stream_in_use));
   }
+  const bool stamped = e->profiling && e->stamps && int(e->stamp_launches.size()) < e->stamp_cap &&
+                       std::strstr(what, "attention") == nullptr && std::strcmp(what, "embed") != 0 &&
+                       std::strcmp(what, "head") != 0;
+  if (stamped) {
+    g_gemm_stamps = e->stamps + size_t(e->stamp_launches.size()) * STAMP_CTAS * GEMM_STAMPS;
+    SAMP_CUDA(cudaMemsetAsync(g_gemm_stamps, 0, size_t(STAMP_CTAS) * GEMM_STAMPS * 8, e->stream_in_use));
+  }
   cudaError_t err = fn();
+  g_gemm_stamps = nullptr;
+  if (stamped) e->stamp_launches.push_back({what, 0});
   if (err == cudaSuccess) err = cudaGetLastError();
   SAMP_REQUIRE(err == cudaSuccess, SAMP_E_DEVICE, std::string(what) + ": " + cudaGetErrorString(err));
   if (e->profiling) {
@@ -780,6 +795,35 @@ extern "C" int samp_sync(samp_engine* e) {
 }
 
 extern "C" int samp_last_launch_count(samp_engine* e) { return e ? e->launches : 0; }
+
+extern "C" int samp_debug_gemm_stamps(samp_engine* e, int max_launches) {
+  return guarded([&] {
+    if (e->stamps) e->mem.release(e->stamps);
+    e->stamps = nullptr;
+    e->stamp_cap = 0;
+    e->stamp_launches.clear();
+    if (max_launches > 0) {
+      e->stamps = e->mem.alloc<unsigned long long>(size_t(max_launches) * STAMP_CTAS * GEMM_STAMPS);
+      e->stamp_cap = max_launches;
+    }
+  });
+}
+
+extern "C" int samp_debug_gemm_stamps_fetch(samp_engine* e, unsigned long long* out, int cap_launches,
+                                            char* names, size_t names_cap, int* n_launches) {
+  return guarded([&] {
+    SAMP_REQUIRE(e->stamps, SAMP_E_CONFIGURATION, "GEMM stamps not enabled");
+    SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));
+    const int n = std::min<int>(cap_launches, int(e->stamp_launches.size()));
+    SAMP_CUDA(cudaMemcpy(out, e->stamps, size_t(n) * STAMP_CTAS * GEMM_STAMPS * 8, cudaMemcpyDeviceToHost));
+    std::string s;
+    for (int i = 0; i < n; ++i) s += e->stamp_launches[i].first + "\n";
+    SAMP_REQUIRE(s.size() < names_cap, SAMP_E_INPUT, "names buffer too small");
+    std::memcpy(names, s.c_str(), s.size() + 1);
+    *n_launches = n;
+    e->stamp_launches.clear();
+  });
+}
 
 extern "C" int samp_set_profiling(samp_engine* e, int on) {
   return guarded([&] {

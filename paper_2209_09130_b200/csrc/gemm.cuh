@@ -69,6 +69,24 @@ __device__ __forceinline__ void epi_bar_sync(int nthreads) {
   asm volatile("bar.sync 1, %0;" :: "r"(nthreads) : "memory");
 }
 
+// Phase stamps (measurement only).  When a launch gets a non-null buffer, CTA b writes
+// GEMM_STAMPS u64 at stamps[b * GEMM_STAMPS]: smid, then %globaltimer (ns) at kernel
+// start, first ring slot full, last ring slot full, accumulator complete, epilogue done,
+// exit.  The host sets g_gemm_stamps before a launch (profiling mode, no graphs).
+constexpr int GEMM_STAMPS = 8, GEMM_STAMP_CTAS = 1024;
+inline unsigned long long* g_gemm_stamps = nullptr;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 // rings <= ~110 KB run two CTAs per SM (register cap ~96); deeper rings one CTA per SM
 template <int BN, int STAGES>
 struct GemmOcc {
@@ -78,7 +96,7 @@ struct GemmOcc {
 template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
 __global__ void __launch_bounds__(64 + 32 * NE, GemmOcc<BN, STAGES>::value)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-            int M, int k_bytes, const typename Epi::Params ep) {
+            int M, int k_bytes, const typename Epi::Params ep, unsigned long long* stamps) {
   using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
   constexpr int TMEM_COLS = tmem_cols_for(BN);
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
@@ -99,6 +117,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const int m0 = blockIdx.y * GEMM_BM;
   const int n0 = blockIdx.x * BN;
   const int nk = k_bytes / 128;
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned long long* stamp = stamps && cta < GEMM_STAMP_CTAS ? stamps + size_t(cta) * GEMM_STAMPS : nullptr;
+  if (stamp && threadIdx.x == 0) {
+    stamp[0] = smid();
+    stamp[1] = globaltimer();
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -117,17 +141,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
   if (warp == 0) {
     if (elect_one()) {
-      for (int kb = 0; kb < nk; ++kb) {
+      // coordinates are in elements: 128 bytes of K = 128 int8 or 64 f16
+      auto kcol = [](int kb) { return KIND == KIND_I8 ? kb * 128 : kb * 64; };
+      // weights (B) do not depend on the previous kernel: fill the ring's B halves
+      // while it drains, then wait for it and stream A
+      const int pre = nk < STAGES ? nk : STAGES;
+      for (int kb = 0; kb < pre; ++kb) {
+        mbar_expect_tx(&full[kb], Lay::A_BYTES + Lay::B_BYTES);
+        tma_load_2d(smem + Lay::B_OFF + kb * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[kb]);
+      }
+      pdl_wait();
+      for (int kb = 0; kb < pre; ++kb)
+        tma_load_2d(smem + Lay::A_OFF + kb * Lay::A_BYTES, &map_a, kcol(kb), m0, &full[kb]);
+      for (int kb = pre; kb < nk; ++kb) {
         const int s = kb % STAGES;
         mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
         mbar_expect_tx(&full[s], Lay::A_BYTES + Lay::B_BYTES);
-        // coordinates are in elements: 128 bytes of K = 128 int8 or 64 f16
-        const int kc = KIND == KIND_I8 ? kb * 128 : kb * 64;
-        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kc, m0, &full[s]);
-        tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kc, n0, &full[s]);
+        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kcol(kb), m0, &full[s]);
+        tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[s]);
       }
     }
     __syncwarp();
@@ -137,6 +170,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int s = kb % STAGES;
         mbar_wait(&full[s], (kb / STAGES) & 1);
         tc_fence_after();
+        if (stamp && (kb == 0 || kb == nk - 1)) stamp[kb == 0 ? 2 : 3] = globaltimer();
         const uint32_t a_base = smem_addr(smem + Lay::A_OFF + s * Lay::A_BYTES);
         const uint32_t b_base = smem_addr(smem + Lay::B_OFF + s * Lay::B_BYTES);
 #pragma unroll
@@ -147,6 +181,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         mma_commit(&empty[s]);
       }
       mma_commit(tmem_full);
+      pdl_trigger();   // last MMA issued: the next kernel's prologue overlaps our epilogue
     }
     __syncwarp();
   } else {
@@ -155,14 +190,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     const int half = NE == 8 ? int(warp - GEMM_EPI_WARP0) / 4 : 0;
     const int tile_row = quarter * 32 + lane_id();
     const int c0 = half * (BN / (NE / 4));
+    pdl_wait();   // residual tiles / outputs belong to earlier kernels
     // idle during the main loop: stage this tile's epilogue operands in smem
     Epi::template prefetch<BN>(ep, epi_smem, m0, n0, M, ep_tid, 32 * NE);
     epi_bar_sync(32 * NE);
     mbar_wait(tmem_full, 0);
     tc_fence_after();
+    if (stamp && ep_tid == 0) stamp[4] = globaltimer();
     EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(c0), m0 + tile_row, tile_row, n0, c0,
              BN / (NE / 4), half, M, ep_tid, 32 * NE};
     Epi::template run<BN, CLUSTER, NE>(ep, c, epi_smem);
+    if (stamp && ep_tid == 0) stamp[5] = globaltimer();
   }
   // non-epilogue warps mirror the epilogue's cluster barriers
   if (warp < GEMM_EPI_WARP0) {
@@ -175,6 +213,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+  if (stamp && threadIdx.x == 0) stamp[6] = globaltimer();
 }
 
 __device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
@@ -765,22 +804,9 @@ inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_
     if (e != cudaSuccess) return e;
     configured_device = dev;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, 1);
-  cfg.blockDim = dim3(64 + 32 * NE, 1, 1);
-  cfg.dynamicSmemBytes = Lay::TOTAL;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  cfg.numAttrs = 0;
-  if (CLUSTER > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CLUSTER;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
-  return cudaLaunchKernelEx(&cfg, kern, map_a, map_b, M, k_bytes, p);
+  unsigned long long* stamps = g_gemm_stamps;
+  return launch_ex(kern, dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, 1), dim3(64 + 32 * NE, 1, 1), Lay::TOTAL, stream,
+                   CLUSTER, map_a, map_b, M, k_bytes, p, stamps);
 }
 
 }  // namespace samp

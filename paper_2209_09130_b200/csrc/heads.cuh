@@ -79,6 +79,8 @@ __device__ __forceinline__ void softmax_argmax(const float* lg, float* pr, int* 
 // order, applies bias + numpy tanh, then the classifier dot products + exact softmax.
 static __global__ void __launch_bounds__(HEAD_THREADS) pooler_kernel(const HeadParams p) {
   extern __shared__ float sh[];           // h [POOL_SEQS][H/4] then partials [8][POOL_SEQS][32]
+  pdl_trigger();
+  pdl_wait();
   const int H = p.hidden_size, KQ = H / POOL_KSPLIT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * POOL_COLS + lane;
@@ -121,6 +123,8 @@ static __global__ void __launch_bounds__(HEAD_THREADS) classifier_kernel(const H
   __shared__ TanhTable tt;
   const int H = p.hidden_size, L = p.num_labels;
   load_tanh_table(&tt, threadIdx.x, HEAD_THREADS);
+  pdl_trigger();
+  pdl_wait();
   __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int s = blockIdx.x * (HEAD_THREADS / 32) + warp;
@@ -148,6 +152,8 @@ static __global__ void __launch_bounds__(HEAD_THREADS) classifier_kernel(const H
 
 // one warp per token
 static __global__ void __launch_bounds__(HEAD_THREADS) tag_kernel(const HeadParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int H = p.hidden_size, L = p.num_labels;
   const int t = blockIdx.x * (HEAD_THREADS / 32) + threadIdx.x / 32;
   if (t >= p.T) return;

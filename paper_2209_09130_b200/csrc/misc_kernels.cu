@@ -15,8 +15,8 @@ static cudaError_t embed_h(const EmbedParams& p, cudaStream_t st) {
     configured = dev;
   }
   constexpr int tok = EMB_THREADS / 32;
-  embed_kernel<H><<<(p.T + tok - 1) / tok, EMB_THREADS, size_t(tok) * H * sizeof(float), st>>>(p);
-  return cudaGetLastError();
+  return launch_ex(embed_kernel<H>, dim3((p.T + tok - 1) / tok), dim3(EMB_THREADS), size_t(tok) * H * sizeof(float),
+                   st, 1, p);
 }
 
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st) {
@@ -43,17 +43,15 @@ cudaError_t launch_classify(const HeadParams& p, cudaStream_t st) {
   }
   const dim3 grid((p.hidden_size + POOL_COLS - 1) / POOL_COLS, (p.nseq + POOL_SEQS - 1) / POOL_SEQS, POOL_KSPLIT);
   const size_t smem = (size_t(POOL_SEQS) * p.hidden_size / POOL_KSPLIT + 8 * POOL_SEQS * 32) * sizeof(float);
-  pooler_kernel<<<grid, HEAD_THREADS, smem, st>>>(p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_ex(pooler_kernel, grid, dim3(HEAD_THREADS), smem, st, 1, p);
   if (e != cudaSuccess) return e;
-  classifier_kernel<<<(p.nseq + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32), HEAD_THREADS,
-                      size_t(HEAD_THREADS / 32) * p.hidden_size * sizeof(float), st>>>(p);
-  return cudaGetLastError();
+  return launch_ex(classifier_kernel, dim3((p.nseq + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32)), dim3(HEAD_THREADS),
+                   size_t(HEAD_THREADS / 32) * p.hidden_size * sizeof(float), st, 1, p);
 }
 
 cudaError_t launch_tag(const HeadParams& p, cudaStream_t st) {
-  tag_kernel<<<(p.T + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32), HEAD_THREADS, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_ex(tag_kernel, dim3((p.T + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32)), dim3(HEAD_THREADS), 0, st,
+                   1, p);
 }
 
 // W [K][N] F32 (archive layout) -> Wt int8 [N][K] (one per-tensor scale, reference

@@ -132,6 +132,8 @@ int samp_debug_gemm_f16(const uint16_t* a, const uint16_t* b, float* c, int m, i
 int samp_debug_quant_exhaustive(const float* scales, int n, unsigned long long* mismatches);
 int samp_debug_div_exhaustive(const float* divisors, int n, unsigned long long* mismatches);
 int samp_debug_exp_exhaustive(unsigned long long* mismatches);
+/* gelu8_finite (FFN1 epilogue fast path) vs the general numpy-exact GELU, all |x| < 1e12 */
+int samp_debug_gelu_finite_exhaustive(unsigned long long* mismatches);
 int samp_debug_unary(int fn, const float* x, float* y, long n);
 
 /* number of kernel launches issued by the last samp_forward (for bench gpu_launches) */

@@ -72,6 +72,28 @@ __global__ void exp_exhaustive_kernel(unsigned long long* bad) {
   atomicAdd(bad, local);
 }
 
+// gelu8_finite against gelu_ref over every float with |x| < 1e12 (the host-proven domain)
+__global__ void gelu_finite_exhaustive_kernel(unsigned long long* bad) {
+  __shared__ TanhTable tt;
+  load_tanh_table(&tt, threadIdx.x, blockDim.x);
+  __syncthreads();
+  unsigned long long local = 0;
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < (1ull << 29);
+       g += uint64_t(gridDim.x) * blockDim.x) {
+    float v[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x[u] = __uint_as_float(uint32_t(g * 8 + u));
+      if (!(fabsf(x[u]) < 1e12f)) x[u] = 0.0f;
+      v[u] = x[u];
+    }
+    gelu8_finite(v, &tt);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) local += __float_as_uint(v[u]) != __float_as_uint(gelu_ref(x[u], &tt));
+  }
+  atomicAdd(bad, local);
+}
+
 __global__ void unary_kernel(int fn, const float* x, float* y, long n) {
   __shared__ TanhTable tt;
   load_tanh_table(&tt, threadIdx.x, blockDim.x);
@@ -125,6 +147,12 @@ extern "C" int samp_debug_div_exhaustive(const float* divisors, int n, unsigned 
 extern "C" int samp_debug_exp_exhaustive(unsigned long long* mismatches) {
   return guarded([&] {
     *mismatches = run_count([](unsigned long long* d) { exp_exhaustive_kernel<<<148 * 8, 256>>>(d); });
+  });
+}
+
+extern "C" int samp_debug_gelu_finite_exhaustive(unsigned long long* mismatches) {
+  return guarded([&] {
+    *mismatches = run_count([](unsigned long long* d) { gelu_finite_exhaustive_kernel<<<148 * 8, 256>>>(d); });
   });
 }
 

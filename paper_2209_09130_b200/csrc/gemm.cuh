@@ -321,15 +321,18 @@ struct EpiQKV {
 };
 
 // FFN1: F32(acc)*mult + b1 -> GELU (numpy/SVML-exact) -> quantize(ffn.mid)
-// (reference encoder.py:406-410)
-struct EpiGeluQuant {
-  struct Params {
-    int8_t* out;
-    int ldo;
-    const float* bias;
-    float mult;
-    float s_out;
-  };
+// (reference encoder.py:406-410).  FINITE: the host proved the GELU argument finite for
+// this launch (gelu8_finite); otherwise the general gelu8 (inf/nan-capable) runs.
+struct GeluQuantParams {
+  int8_t* out;
+  int ldo;
+  const float* bias;
+  float mult;
+  float s_out;
+};
+template <bool FINITE>
+struct EpiGeluQuantT {
+  using Params = GeluQuantParams;
   template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
   template <int BN>
@@ -361,7 +364,8 @@ struct EpiGeluQuant {
         float v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
-        gelu8(v, tt);
+        if constexpr (FINITE) gelu8_finite(v, tt);
+        else gelu8(v, tt);
         w[g / 4] = pack4_i8(quant_bounded(v[0], rq), quant_bounded(v[1], rq), quant_bounded(v[2], rq), quant_bounded(v[3], rq));
         w[g / 4 + 1] = pack4_i8(quant_bounded(v[4], rq), quant_bounded(v[5], rq), quant_bounded(v[6], rq), quant_bounded(v[7], rq));
       }
@@ -369,6 +373,9 @@ struct EpiGeluQuant {
     }
   }
 };
+
+using EpiGeluQuant = EpiGeluQuantT<false>;
+using EpiGeluQuantFinite = EpiGeluQuantT<true>;
 
 // FP16-path bias (+ optional GELU) epilogue: acc(F32) + bias [-> gelu] -> f16 storage.
 // (reference mha_fp encoder.py:291-292 qkv = gemm + qkv_b; ffn_fp :325-326 gelu(mid))

@@ -1,9 +1,23 @@
+#include "gemm_persistent.cuh"
 #include "kernels.h"
 
 namespace samp {
 
+#ifndef SAMP_PERSIST_NE
+#define SAMP_PERSIST_NE 8
+#endif
+
 cudaError_t gemm_f16out(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                         const EpiF16Out::Params& p, cudaStream_t st) {
+  constexpr int NEP = SAMP_PERSIST_NE;
+  if (std::getenv("SAMP_NO_PERSISTENT") == nullptr) {
+    switch (bn) {
+      case 256: return launch_gemm_persistent<KIND_F16, 256, 4, NEP, EpiF16Out>(a, b, M, N, kb, p, st);
+      case 128: return launch_gemm_persistent<KIND_F16, 128, 5, NEP, EpiF16Out>(a, b, M, N, kb, p, st);
+      case 64: return launch_gemm_persistent<KIND_F16, 64, 6, 8, EpiF16Out>(a, b, M, N, kb, p, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (bn) {
     case 256: return launch_gemm<KIND_F16, 256, 2, 1, 8, EpiF16Out>(a, b, M, N, kb, p, st);
     case 128: return launch_gemm<KIND_F16, 128, 3, 1, 8, EpiF16Out>(a, b, M, N, kb, p, st);

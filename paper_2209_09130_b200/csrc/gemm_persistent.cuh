@@ -1,0 +1,214 @@
+// Persistent warp-specialised tcgen05 GEMM for the row-local epilogues (QKV quantize,
+// FFN1 GELU+quantize, f16 bias/GELU outputs).
+//
+// Why: the one-tile-per-CTA kernel (gemm.cuh) runs each CTA's epilogue strictly after its
+// own main loop, and co-resident CTAs start in the same phase, so at 768 FFN1 tiles the
+// SMs alternate between "everyone loads" and "everyone runs GELU" over 2.6 waves
+// (tools/gemm_phases.py: 8.7 us per tile, 5.5 us of it epilogue).  Here one CTA per SM
+// walks a static tile list with TWO TMEM accumulators: the MMA warp fills buffer j&1 for
+// tile j while the epilogue warps drain tile j-1 from the other buffer, so per SM the
+// time is ~max(sum of epilogues, sum of main loops) instead of their sum.
+//
+// Roles (64 + 32*NE threads, 1 CTA / SM):
+//   warp 0      TMA producer over the flat (tile, k-block) sequence; the first tile's
+//               weight (B) boxes are issued before griddepcontrol.wait (PDL)
+//   warp 1      TMEM allocator (2*BN columns) + MMA issuer; acc_full[b] / acc_empty[b]
+//   warps 2..   NE epilogue warps (NE = 8 or 16): warp w reads TMEM lane quarter w%4 and
+//               column part (w-2)/4 of BN; per tile they stage the NEXT tile's bias with
+//               cp.async into the other of two epilogue smem buffers (the read-only tanh
+//               table is loaded once per buffer at start).
+// The epilogue structs are the ones of gemm.cuh (same run(), bit-identical results); their
+// smem layout ends with the BN bias floats, which is what the per-tile staging rewrites.
+#pragma once
+#include "gemm.cuh"
+
+namespace samp {
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int BN, int STAGES, int EPI_BYTES>
+struct PersistLayout {
+  static constexpr int A_BYTES = GEMM_BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int A_OFF = 0;
+  static constexpr int B_OFF = STAGES * A_BYTES;
+  static constexpr int BAR_OFF = B_OFF + STAGES * B_BYTES;             // full, empty, acc_full[2], acc_empty[2]
+  static constexpr int EPI_STRIDE = (EPI_BYTES + 127) & ~127;
+  static constexpr int EPI_OFF = (BAR_OFF + 8 * (2 * STAGES + 4) + 8 + 127) & ~127;
+  static constexpr int TOTAL = EPI_OFF + 2 * EPI_STRIDE + 1024;
+};
+
+template <int KIND, int BN, int STAGES, int NE, class Epi>
+__global__ void __launch_bounds__(64 + 32 * NE, 1)
+gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       int M, int N, int k_bytes, const typename Epi::Params ep) {
+  using Lay = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
+  constexpr int TMEM_COLS = tmem_cols_for(2 * BN);
+  constexpr int PARTS = NE / 4;
+  constexpr int EPI_BIAS_OFF = Epi::template smem_bytes<BN>() - BN * 4;
+  constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
+  static_assert(2 * BN <= 512 && BN % 16 == 0, "two accumulators must fit TMEM");
+  static_assert(NE == 8 || NE == 16, "epilogue warps");
+  static_assert((BN / PARTS) % 16 == 0, "epilogue column chunks");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint8_t* epi_smem = smem + Lay::EPI_OFF;
+
+  const uint32_t warp = warp_id();
+  const int mtiles = (M + GEMM_BM - 1) / GEMM_BM;
+  const int ntiles = mtiles * (N / BN);
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  const int nk = k_bytes / 128;
+  auto tile_m0 = [&](int j) { return ((int(blockIdx.x) + j * int(gridDim.x)) % mtiles) * GEMM_BM; };
+  auto tile_n0 = [&](int j) { return ((int(blockIdx.x) + j * int(gridDim.x)) / mtiles) * BN; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], NE);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one() && my_tiles > 0) {
+      auto kcol = [](int kb) { return KIND == KIND_I8 ? kb * 128 : kb * 64; };
+      const int total = my_tiles * nk;
+      const int pre = nk < STAGES ? nk : STAGES;   // first tile's weights before the PDL wait
+      const int n00 = tile_n0(0);
+      for (int kb = 0; kb < pre; ++kb) {
+        mbar_expect_tx(&full[kb], Lay::A_BYTES + Lay::B_BYTES);
+        tma_load_2d(smem + Lay::B_OFF + kb * Lay::B_BYTES, &map_b, kcol(kb), n00, &full[kb]);
+      }
+      pdl_wait();
+      const int m00 = tile_m0(0);
+      for (int kb = 0; kb < pre; ++kb)
+        tma_load_2d(smem + Lay::A_OFF + kb * Lay::A_BYTES, &map_a, kcol(kb), m00, &full[kb]);
+      for (int it = pre; it < total; ++it) {
+        const int j = it / nk, kb = it - j * nk;
+        const int s = it % STAGES;
+        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], Lay::A_BYTES + Lay::B_BYTES);
+        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kcol(kb), tile_m0(j), &full[s]);
+        tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), tile_n0(j), &full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      int it = 0;
+      for (int j = 0; j < my_tiles; ++j) {
+        const int b = j & 1;
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + uint32_t(b * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_addr(smem + Lay::A_OFF + s * Lay::A_BYTES);
+          const uint32_t b_base = smem_addr(smem + Lay::B_OFF + s * Lay::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_ss<KIND>(d, sdesc_k_sw128(a_base + 32 * k), sdesc_k_sw128(b_base + 32 * k), IDESC, (kb | k) != 0);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[b]);
+      }
+      pdl_trigger();   // last MMA issued: the next kernel's prologue overlaps our epilogues
+    }
+    __syncwarp();
+  } else {
+    const int ep_tid = threadIdx.x - GEMM_EPI_WARP0 * 32;
+    const int quarter = warp & 3;
+    const int part = int(warp - GEMM_EPI_WARP0) / 4;
+    const int tile_row = quarter * 32 + lane_id();
+    const int c0 = part * (BN / PARTS);
+    pdl_wait();
+    // both buffers: read-only tables + the first two tiles' bias
+    for (int b = 0; b < 2 && b < my_tiles; ++b)
+      Epi::template prefetch<BN>(ep, epi_smem + b * Lay::EPI_STRIDE, tile_m0(b), tile_n0(b), M, ep_tid, 32 * NE);
+    epi_bar_sync(32 * NE);
+    for (int j = 0; j < my_tiles; ++j) {
+      const int b = j & 1;
+      // stage tile j+1's bias into the other buffer (its last reader, tile j-1, is done)
+      if (j >= 1 && j + 1 < my_tiles) {
+        float* dst = reinterpret_cast<float*>(epi_smem + ((j + 1) & 1) * Lay::EPI_STRIDE + EPI_BIAS_OFF);
+        const float* src = ep.bias + tile_n0(j + 1);
+        for (int i = ep_tid; i < BN / 4; i += 32 * NE) cp_async16(dst + 4 * i, src + 4 * i);
+        cp_async_commit();
+      }
+      mbar_wait(&acc_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const int m0 = tile_m0(j);
+      EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * BN + c0), m0 + tile_row, tile_row, tile_n0(j), c0,
+               BN / PARTS, part, M, ep_tid, 32 * NE};
+      Epi::template run<BN, 1, NE>(ep, c, epi_smem + b * Lay::EPI_STRIDE);
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
+      cp_async_wait_all();
+      epi_bar_sync(32 * NE);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+inline int device_sm_count() {
+  static thread_local int dev = -1, count = 0;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d != dev) {
+    cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, d);
+    dev = d;
+  }
+  return count;
+}
+
+template <int KIND, int BN, int STAGES, int NE, class Epi>
+inline cudaError_t launch_gemm_persistent(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N,
+                                          int k_bytes, const typename Epi::Params& p, cudaStream_t stream) {
+  using Lay = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
+  auto kern = gemm_persistent_kernel<KIND, BN, STAGES, NE, Epi>;
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured = dev;
+  }
+  const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * (N / BN);
+  const int grid = tiles < device_sm_count() ? tiles : device_sm_count();
+  return launch_ex(kern, dim3(grid), dim3(64 + 32 * NE), Lay::TOTAL, stream, 1, map_a, map_b, M, N, k_bytes, p);
+}
+
+}  // namespace samp

@@ -17,7 +17,8 @@ struct Tiles {
 // gemm_i8.cu
 cudaError_t gemm_qkv_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                         const EpiQKV::Params& p, cudaStream_t st);
-cudaError_t gemm_gelu_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+// finite: |acc*mult + bias| is bounded well below the GELU overflow (host check)
+cudaError_t gemm_gelu_i8(int bn, bool finite, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                          const EpiGeluQuant::Params& p, cudaStream_t st);
 // gemm_ln.cu
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,

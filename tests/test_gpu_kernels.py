@@ -93,6 +93,14 @@ def test_exp_fast_division_exhaustive():
     assert bad.value == 0
 
 
+def test_gelu_finite_fast_path_exhaustive():
+    import ctypes
+    lib = _lib.load()
+    bad = ctypes.c_ulonglong()
+    _lib.check(lib.samp_debug_gelu_finite_exhaustive(ctypes.byref(bad)))
+    assert bad.value == 0
+
+
 @pytest.mark.parametrize("fn,name", [(0, "np_exp"), (1, "np_tanh")])
 def test_device_transcendentals_equal_oracle(fn, name):
     lib = _lib.load()

@@ -299,12 +299,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         } else {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
-            int q[4];
+            float q[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              q[u] = (c0 + j + u) < S ? quant_bounded(div_fast(__uint_as_float(v[j + u]), rden), rsm) : 0;
-            w[j / 4] = (uint32_t(q[0]) & 0xff) | ((uint32_t(q[1]) & 0xff) << 8) |
-                       ((uint32_t(q[2]) & 0xff) << 16) | ((uint32_t(q[3]) & 0xff) << 24);
+              q[u] = (c0 + j + u) < S ? quant_pre_bounded(div_fast(__uint_as_float(v[j + u]), rden), rsm) : 0.0f;
+            w[j / 4] = trunc_pack4_s8(q[0], q[1], q[2], q[3]);
           }
         }
         // 32 keys = 32 (int8) or 64 (f16) bytes: 2 or 4 swizzled 16-byte chunks
@@ -350,11 +349,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         uint32_t w[8];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          int q[4];
+          float q[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) q[u] = quant_bounded(__fmul_rn(__int2float_rn(int(o[j + u])), p.mult_ctx), rctx);
-          w[j / 4] = (uint32_t(q[0]) & 0xff) | ((uint32_t(q[1]) & 0xff) << 8) |
-                     ((uint32_t(q[2]) & 0xff) << 16) | ((uint32_t(q[3]) & 0xff) << 24);
+          for (int u = 0; u < 4; ++u) q[u] = quant_pre_bounded(__fmul_rn(__int2float_rn(int(o[j + u])), p.mult_ctx), rctx);
+          w[j / 4] = trunc_pack4_s8(q[0], q[1], q[2], q[3]);
         }
         reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
         reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);

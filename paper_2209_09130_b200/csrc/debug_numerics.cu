@@ -36,7 +36,15 @@ __global__ void quant_exhaustive_kernel(const float* scales, int n, unsigned lon
       if (x != x) continue;  // NaN codes are unspecified in the reference (clip keeps NaN)
       const int want = quant_i8(x, s);
       local += quant_fast(x, r) != want;
-      if (fabsf(x) < 1.1529215e18f) local += quant_bounded(x, r) != want;   // |x| < 2^60
+      const bool bounded = fabsf(x) < 1.1529215e18f;   // |x| < 2^60
+      if (bounded) local += quant_bounded(x, r) != want;
+      // packed path: byte 0 = x, byte 1 = -x, byte 2 = 0, byte 3 = x (bounded variant when legal)
+      const uint32_t pk = trunc_pack4_s8(quant_pre_fast(x, r), quant_pre_fast(-x, r), 0.0f,
+                                         bounded ? quant_pre_bounded(x, r) : quant_pre_fast(x, r));
+      local += int(int8_t(pk & 0xffu)) != want;
+      local += int(int8_t((pk >> 8) & 0xffu)) != quant_i8(-x, s);
+      local += ((pk >> 16) & 0xffu) != 0u;
+      local += int(int8_t(pk >> 24)) != want;
     }
   }
   atomicAdd(bad, local);

@@ -187,8 +187,8 @@ static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedPa
           make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
     }
     if (p.out_i8) {
-      const uint32_t wv = (uint32_t(quant_fast(y[0], rq)) & 0xff) | ((uint32_t(quant_fast(y[1], rq)) & 0xff) << 8) |
-                          ((uint32_t(quant_fast(y[2], rq)) & 0xff) << 16) | (uint32_t(quant_fast(y[3], rq)) << 24);
+      const uint32_t wv = trunc_pack4_s8(quant_pre_fast(y[0], rq), quant_pre_fast(y[1], rq),
+                                         quant_pre_fast(y[2], rq), quant_pre_fast(y[3], rq));
       *reinterpret_cast<uint32_t*>(p.out_i8 + base + c) = wv;
     }
   }

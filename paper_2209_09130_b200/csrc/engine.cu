@@ -65,13 +65,30 @@ struct LayerDev {
   float *b1 = nullptr, *b2 = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
   double s_w[6] = {0, 0, 0, 0, 0, 0};  // qw kw vw ow w1 w2
   double b1_absmax = 0;                 // max|b1|: bounds the FFN1 GELU argument
-  CUtensorMap m_qkv_i8, m_wo_i8, m_w1_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w1_f16, m_w2_f16;
+  CUtensorMap m_qkv_i8, m_wo_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w2_f16;
+  CUtensorMap m_w1_i8[3], m_w1_f16[3];   // FFN1 B operand, box rows FFN1_BN[k]
 };
 
 static int pick_bn(int n) {
   for (int bn : {256, 128, 64})
     if (n % bn == 0) return bn;
   return 0;
+}
+
+// FFN1 runs persistent (one CTA per SM walking tiles); its makespan is the per-CTA tile
+// count times the tile width, so the width is picked per launch from these
+constexpr int FFN1_BN[3] = {64, 96, 128};
+static int ffn1_bn_index(int T, int I, int sms, bool allow96 = true) {
+  const int mt = (T + GEMM_BM - 1) / GEMM_BM;
+  int best = -1;
+  long best_cost = 0;
+  for (int k = 0; k < 3; ++k) {
+    if (I % FFN1_BN[k] || (!allow96 && FFN1_BN[k] == 96)) continue;
+    const long tiles = long(mt) * (I / FFN1_BN[k]);
+    const long cost = (tiles + sms - 1) / sms * FFN1_BN[k];
+    if (best < 0 || cost <= best_cost) best = k, best_cost = cost;   // ties: wider tile
+  }
+  return best;
 }
 
 static Tiles choose_tiles(int H, int I) {
@@ -133,6 +150,7 @@ struct samp_engine {
   std::map<std::string, std::vector<uint8_t>> stages;
   std::vector<int> h_pos;
   bool profiling = false;
+  int sms = 148;                  // SM count of the engine's device
   // GEMM phase stamps (profiling mode): [stamp_cap launches][STAMP_CTAS][GEMM_STAMPS]
   unsigned long long* stamps = nullptr;
   int stamp_cap = 0;
@@ -479,7 +497,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     // |x| <= K * 128^2 * |mult| + max|b1| far below where C*(x + K x^3) overflows: the
     // GELU's inf/nan path is unreachable (gelu8_finite)
     const bool finite = double(H) * 16384.0 * std::fabs(double(gp.mult)) + w.b1_absmax < 1e12;
-    check_launch(e, gemm_gelu_i8(t.bn_ffn1, finite, a.a_ffn_in, w.m_w1_i8, T, I, H, gp, st), "ffn1_i8");
+    const int k1 = ffn1_bn_index(T, I, e->sms);
+    check_launch(e, gemm_gelu_i8(FFN1_BN[k1], finite, a.a_ffn_in, w.m_w1_i8[k1], T, I, H, gp, st), "ffn1_i8");
     record(e, "mid_q", i, a.mid_i8, size_t(T) * I);
     lp.res_i8 = a.ffn_in_i8;
     lp.res_scale = f32(s_fin);
@@ -487,7 +506,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     check_launch(e, gemm_ln_i8(t, a.a_mid_i8, w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
   } else {
     EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
-    check_launch(e, gemm_f16out(t.bn_ffn1, a.a_ln1_f16, w.m_w1_f16, T, I, 2 * H, gp, st), "ffn1_f16");
+    const int k1 = ffn1_bn_index(T, I, e->sms, false);   // EpiF16Out walks 32-column chunks
+    check_launch(e, gemm_f16out(FFN1_BN[k1], a.a_ln1_f16, w.m_w1_f16[k1], T, I, 2 * H, gp, st), "ffn1_f16");
     lp.res_f32 = a.ln1_f32;
     lp.acc_is_f32 = 1;
     lp.f16_round = (p == SAMP_LAYER_FP) ? fp16_store : 0;
@@ -590,6 +610,7 @@ extern "C" int samp_engine_create(const samp_model_desc* desc, int device, samp_
     e->d = d;
     e->device = device;
     e->tiles = t;
+    cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device);
     e->layers.resize(d.num_layers);
     if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
       delete e;
@@ -681,11 +702,14 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     const Tiles& tl = e->tiles;
     w.m_qkv_i8 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, tl.bn_qkv);
     w.m_wo_i8 = tmap_i8(w.wo_i8, H, H, H, 128, tl.bn_ln);
-    w.m_w1_i8 = tmap_i8(w.w1_i8, I, H, H, 128, tl.bn_ffn1);
+    for (int k = 0; k < 3; ++k)
+      if (I % FFN1_BN[k] == 0) {
+        w.m_w1_i8[k] = tmap_i8(w.w1_i8, I, H, H, 128, FFN1_BN[k]);
+        w.m_w1_f16[k] = tmap_f16(w.w1_f16, I, H, H, 64, FFN1_BN[k]);
+      }
     w.m_w2_i8 = tmap_i8(w.w2_i8, H, I, I, 128, tl.bn_ln);
     w.m_qkv_f16 = tmap_f16(w.qkv_f16, 3 * H, H, H, 64, tl.bn_qkv);
     w.m_wo_f16 = tmap_f16(w.wo_f16, H, H, H, 64, tl.bn_ln);
-    w.m_w1_f16 = tmap_f16(w.w1_f16, I, H, H, 64, tl.bn_ffn1);
     w.m_w2_f16 = tmap_f16(w.w2_f16, H, I, I, 64, tl.bn_ln);
     w.loaded = true;
   });

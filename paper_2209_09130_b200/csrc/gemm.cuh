@@ -229,6 +229,15 @@ __device__ __forceinline__ void store32_i8(int8_t* dst, const int (&q)[32]) {
   reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
+// 32 pre-rounded quantize values (quant_pre_*) -> 32 int8 codes at dst
+__device__ __forceinline__ void store32_pre(int8_t* dst, const float (&v)[32]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = trunc_pack4_s8(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 __device__ __forceinline__ void load_bias32(const float* b, float (&out)[32]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -311,11 +320,11 @@ struct EpiQKV {
       float b[32];
       load_smem32(sbias + c.c0 + col, b);
       tmem_wait_ld();
-      int q[32];
+      float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        q[j] = quant_bounded(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j])), mult), b[j]), rq);
-      if (c.row < c.M) store32_i8(p.out + size_t(c.row) * p.ldo + gcol, q);
+        v[j] = quant_pre_bounded(__fadd_rn(__fmul_rn(__int2float_rn(int(r[j])), mult), b[j]), rq);
+      if (c.row < c.M) store32_pre(p.out + size_t(c.row) * p.ldo + gcol, v);
     }
   }
 };
@@ -345,31 +354,42 @@ struct EpiGeluQuantT {
     const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
     const float* sbias = reinterpret_cast<const float*>(smem + sizeof(TanhTable));
     const Recip rq = make_recip(p.s_out);
-    // 16 columns per step keeps the 8-wide batched table lookups under the 96-register cap
+    // CH columns per TMEM load: 16 keeps the one-tile kernel under its 96-register cap
+#ifndef SAMP_GELU_CHUNK
+#define SAMP_GELU_CHUNK 16
+#endif
+    constexpr int CH = (BN / (NE / 4)) % SAMP_GELU_CHUNK == 0 ? SAMP_GELU_CHUNK : 16;
 #pragma unroll 1
-    for (int col = 0; col < c.ncols; col += 16) {
+    for (int col = 0; col < c.ncols; col += CH) {
       const int gcol = c.n0 + c.c0 + col;
-      uint32_t r[16];
-      tmem_ld16(c.taddr + col, r);
-      float b[16];
+      uint32_t r[CH];
+      if constexpr (CH == 32) tmem_ld32(c.taddr + col, r);
+      else tmem_ld16(c.taddr + col, r);
+      float b[CH];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < CH / 4; ++j) {
         const float4 v = reinterpret_cast<const float4*>(sbias + c.c0 + col)[j];
         b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
       }
       tmem_wait_ld();
-      uint32_t w[4];
+      uint32_t w[CH / 4];
 #pragma unroll
-      for (int g = 0; g < 16; g += 8) {
+      for (int g = 0; g < CH; g += 8) {
         float v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
         if constexpr (FINITE) gelu8_finite(v, tt);
         else gelu8(v, tt);
-        w[g / 4] = pack4_i8(quant_bounded(v[0], rq), quant_bounded(v[1], rq), quant_bounded(v[2], rq), quant_bounded(v[3], rq));
-        w[g / 4 + 1] = pack4_i8(quant_bounded(v[4], rq), quant_bounded(v[5], rq), quant_bounded(v[6], rq), quant_bounded(v[7], rq));
+        w[g / 4] = trunc_pack4_s8(quant_pre_bounded(v[0], rq), quant_pre_bounded(v[1], rq),
+                                  quant_pre_bounded(v[2], rq), quant_pre_bounded(v[3], rq));
+        w[g / 4 + 1] = trunc_pack4_s8(quant_pre_bounded(v[4], rq), quant_pre_bounded(v[5], rq),
+                                      quant_pre_bounded(v[6], rq), quant_pre_bounded(v[7], rq));
       }
-      if (c.row < c.M) *reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (c.row < c.M) {
+        uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
+#pragma unroll
+        for (int q = 0; q < CH / 16; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      }
     }
   }
 };
@@ -531,15 +551,18 @@ struct EpiResLN {
 
   // emit 32 normalised values (quantize / deq / f16 round / amax / stores)
   __device__ static void emit32(const Params& p, size_t rbase, int gcol, const Recip& rq, float (&y)[32], float& amx) {
-    if (p.out_i8 || p.deq_outputs) {
+    if (p.deq_outputs) {
       int q[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) q[j] = quant_fast(y[j], rq);
       if (p.out_i8) store32_i8(p.out_i8 + rbase + gcol, q);
-      if (p.deq_outputs) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
-      }
+      for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
+    } else if (p.out_i8) {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = quant_pre_fast(y[j], rq);
+      store32_pre(p.out_i8 + rbase + gcol, v);
     }
     if (p.f16_round) {
 #pragma unroll
@@ -756,15 +779,18 @@ struct EpiResLN {
       for (int j = 0; j < 32; ++j)
         y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(__uint_as_float(r[j]), mean), inv), g[j]), be[j]);
       if (!valid) continue;
-      if (p.out_i8 || p.deq_outputs) {
+      if (p.deq_outputs) {
         int q[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) q[j] = quant_fast(y[j], rq);
         if (p.out_i8) store32_i8(p.out_i8 + rbase + gcol, q);
-        if (p.deq_outputs) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
-        }
+        for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
+      } else if (p.out_i8) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = quant_pre_fast(y[j], rq);
+        store32_pre(p.out_i8 + rbase + gcol, v);
       }
       if (p.f16_round) {
 #pragma unroll

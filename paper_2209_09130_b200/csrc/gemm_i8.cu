@@ -3,6 +3,9 @@
 
 namespace samp {
 
+#ifndef SAMP_PERSIST_STAGES128
+#define SAMP_PERSIST_STAGES128 5
+#endif
 #ifndef SAMP_PERSIST_NE
 #define SAMP_PERSIST_NE 8
 #endif
@@ -20,7 +23,8 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
   if (persistent && persistent_enabled()) {
     switch (bn) {
       case 256: return launch_gemm_persistent<KIND_I8, 256, 4, NEP, Epi>(a, b, M, N, kb, p, st);
-      case 128: return launch_gemm_persistent<KIND_I8, 128, 5, NEP, Epi>(a, b, M, N, kb, p, st);
+      case 128: return launch_gemm_persistent<KIND_I8, 128, SAMP_PERSIST_STAGES128, NEP, Epi>(a, b, M, N, kb, p, st);
+      case 96: return launch_gemm_persistent<KIND_I8, 96, 6, 8, Epi>(a, b, M, N, kb, p, st);
       case 64: return launch_gemm_persistent<KIND_I8, 64, 6, 8, Epi>(a, b, M, N, kb, p, st);
     }
     return cudaErrorInvalidValue;

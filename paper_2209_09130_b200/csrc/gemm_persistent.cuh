@@ -42,10 +42,13 @@ struct PersistLayout {
   static constexpr int TOTAL = EPI_OFF + 2 * EPI_STRIDE + 1024;
 };
 
+#ifndef SAMP_PERSIST_CTAS
+#define SAMP_PERSIST_CTAS 1
+#endif
 template <int KIND, int BN, int STAGES, int NE, class Epi>
-__global__ void __launch_bounds__(64 + 32 * NE, 1)
+__global__ void __launch_bounds__(64 + 32 * NE, SAMP_PERSIST_CTAS)
 gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                       int M, int N, int k_bytes, const typename Epi::Params ep) {
+                       int M, int N, int k_bytes, const typename Epi::Params ep, unsigned long long* stamps) {
   using Lay = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
   constexpr int TMEM_COLS = tmem_cols_for(2 * BN);
   constexpr int PARTS = NE / 4;
@@ -71,6 +74,12 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
   const int nk = k_bytes / 128;
   auto tile_m0 = [&](int j) { return ((int(blockIdx.x) + j * int(gridDim.x)) % mtiles) * GEMM_BM; };
   auto tile_n0 = [&](int j) { return ((int(blockIdx.x) + j * int(gridDim.x)) / mtiles) * BN; };
+  // phase stamps (measurement): CTA b < 64, tile j < 16 -> stamps[(b*16 + j)*8 + f]:
+  // f0 epilogue starts waiting, f1 accumulator ready, f2 epilogue done, f3 MMA starts
+  // (buffer free), f4 last MMA of the tile issued, f5 producer issues the tile's first box
+  auto stamp = [&](int j, int f) {
+    if (stamps && blockIdx.x < 64 && j < 16) stamps[(blockIdx.x * 16 + j) * 8 + f] = globaltimer();
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -99,6 +108,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
       const int total = my_tiles * nk;
       const int pre = nk < STAGES ? nk : STAGES;   // first tile's weights before the PDL wait
       const int n00 = tile_n0(0);
+      stamp(0, 5);
       for (int kb = 0; kb < pre; ++kb) {
         mbar_expect_tx(&full[kb], Lay::A_BYTES + Lay::B_BYTES);
         tma_load_2d(smem + Lay::B_OFF + kb * Lay::B_BYTES, &map_b, kcol(kb), n00, &full[kb]);
@@ -111,6 +121,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         const int j = it / nk, kb = it - j * nk;
         const int s = it % STAGES;
         mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        if (kb == 0) stamp(j, 5);
         mbar_expect_tx(&full[s], Lay::A_BYTES + Lay::B_BYTES);
         tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kcol(kb), tile_m0(j), &full[s]);
         tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), tile_n0(j), &full[s]);
@@ -124,6 +135,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         const int b = j & 1;
         mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
+        stamp(j, 3);
         const uint32_t d = tmem + uint32_t(b * BN);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
@@ -137,6 +149,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
           mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[b]);
+        stamp(j, 4);
       }
       pdl_trigger();   // last MMA issued: the next kernel's prologue overlaps our epilogues
     }
@@ -161,8 +174,10 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         for (int i = ep_tid; i < BN / 4; i += 32 * NE) cp_async16(dst + 4 * i, src + 4 * i);
         cp_async_commit();
       }
+      if (ep_tid == 0) stamp(j, 0);
       mbar_wait(&acc_full[b], (j >> 1) & 1);
       tc_fence_after();
+      if (ep_tid == 0) stamp(j, 1);
       const int m0 = tile_m0(j);
       EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * BN + c0), m0 + tile_row, tile_row, tile_n0(j), c0,
                BN / PARTS, part, M, ep_tid, 32 * NE};
@@ -172,6 +187,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
       if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
       cp_async_wait_all();
       epi_bar_sync(32 * NE);
+      if (ep_tid == 0) stamp(j, 2);
     }
   }
   tc_fence_before();
@@ -207,8 +223,11 @@ inline cudaError_t launch_gemm_persistent(const CUtensorMap& map_a, const CUtens
     configured = dev;
   }
   const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * (N / BN);
-  const int grid = tiles < device_sm_count() ? tiles : device_sm_count();
-  return launch_ex(kern, dim3(grid), dim3(64 + 32 * NE), Lay::TOTAL, stream, 1, map_a, map_b, M, N, k_bytes, p);
+  const int slots = device_sm_count() * SAMP_PERSIST_CTAS;
+  const int grid = tiles < slots ? tiles : slots;
+  unsigned long long* stamps = g_gemm_stamps;
+  return launch_ex(kern, dim3(grid), dim3(64 + 32 * NE), Lay::TOTAL, stream, 1, map_a, map_b, M, N, k_bytes, p,
+                   stamps);
 }
 
 }  // namespace samp

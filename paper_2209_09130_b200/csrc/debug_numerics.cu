@@ -25,7 +25,7 @@ __device__ __forceinline__ float np_expf_ieee(float x) {  // np_expf with __fdiv
   return scale_pow2(__fdiv_rn(num, den), static_cast<int>(k));
 }
 
-__global__ void quant_exhaustive_kernel(const float* scales, int n, unsigned long long* bad) {
+__global__ void quant_exhaustive_kernel(const float* scales, int n, unsigned long long* bad, const X2 k) {
   unsigned long long local = 0;
   for (int si = 0; si < n; ++si) {
     const float s = scales[si];
@@ -45,6 +45,11 @@ __global__ void quant_exhaustive_kernel(const float* scales, int n, unsigned lon
       local += int(int8_t((pk >> 8) & 0xffu)) != quant_i8(-x, s);
       local += ((pk >> 16) & 0xffu) != 0u;
       local += int(int8_t(pk >> 24)) != want;
+      if (bounded) {   // FFMA2 pair form (x, -x)
+        const float2 q2 = quant_pre2(f2(x, -x), r, k);
+        const uint32_t p2 = trunc_pack4_s8(q2.x, q2.y, 0.0f, 0.0f);
+        local += (int(int8_t(p2 & 0xffu)) != want) + (int(int8_t((p2 >> 8) & 0xffu)) != quant_i8(-x, s));
+      }
     }
   }
   atomicAdd(bad, local);
@@ -80,8 +85,9 @@ __global__ void exp_exhaustive_kernel(unsigned long long* bad) {
   atomicAdd(bad, local);
 }
 
-// gelu8_finite against gelu_ref over every float with |x| < 1e12 (the host-proven domain)
-__global__ void gelu_finite_exhaustive_kernel(unsigned long long* bad) {
+// gelu8_finite (and its FFMA2 form) against gelu_ref over every float with |x| < 1e12
+// (the host-proven domain)
+__global__ void gelu_finite_exhaustive_kernel(unsigned long long* bad, const X2 k) {
   __shared__ TanhTable tt;
   load_tanh_table(&tt, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -95,9 +101,16 @@ __global__ void gelu_finite_exhaustive_kernel(unsigned long long* bad) {
       if (!(fabsf(x[u]) < 1e12f)) x[u] = 0.0f;
       v[u] = x[u];
     }
-    gelu8_finite(v, &tt);
+    float v2[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) local += __float_as_uint(v[u]) != __float_as_uint(gelu_ref(x[u], &tt));
+    for (int u = 0; u < 8; ++u) v2[u] = v[u];
+    gelu8_finite(v, &tt);
+    gelu8_finite_x2(v2, &tt, k);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t want = __float_as_uint(gelu_ref(x[u], &tt));
+      local += (__float_as_uint(v[u]) != want) + (__float_as_uint(v2[u]) != want);
+    }
   }
   atomicAdd(bad, local);
 }
@@ -137,7 +150,7 @@ extern "C" int samp_debug_quant_exhaustive(const float* scales, int n, unsigned 
     SAMP_CUDA(cudaMalloc(&g_vals, n * sizeof(float)));
     SAMP_CUDA(cudaMemcpy(g_vals, scales, n * sizeof(float), cudaMemcpyHostToDevice));
     g_n = n;
-    *mismatches = run_count([](unsigned long long* d) { quant_exhaustive_kernel<<<148 * 8, 256>>>(g_vals, g_n, d); });
+    *mismatches = run_count([](unsigned long long* d) { quant_exhaustive_kernel<<<148 * 8, 256>>>(g_vals, g_n, d, x2_consts()); });
     cudaFree(g_vals);
   });
 }
@@ -160,7 +173,7 @@ extern "C" int samp_debug_exp_exhaustive(unsigned long long* mismatches) {
 
 extern "C" int samp_debug_gelu_finite_exhaustive(unsigned long long* mismatches) {
   return guarded([&] {
-    *mismatches = run_count([](unsigned long long* d) { gelu_finite_exhaustive_kernel<<<148 * 8, 256>>>(d); });
+    *mismatches = run_count([](unsigned long long* d) { gelu_finite_exhaustive_kernel<<<148 * 8, 256>>>(d, x2_consts()); });
   });
 }
 

@@ -338,6 +338,7 @@ struct GeluQuantParams {
   const float* bias;
   float mult;
   float s_out;
+  X2 k = x2_consts();   // opaque FFMA2 constants (packed path)
 };
 template <bool FINITE>
 struct EpiGeluQuantT {
@@ -376,14 +377,31 @@ struct EpiGeluQuantT {
 #pragma unroll
       for (int g = 0; g < CH; g += 8) {
         float v[8];
+        if constexpr (FINITE) {   // packed (FFMA2) arithmetic, see numerics.cuh
+          const X2 k = p.k;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
-        if constexpr (FINITE) gelu8_finite(v, tt);
-        else gelu8(v, tt);
-        w[g / 4] = trunc_pack4_s8(quant_pre_bounded(v[0], rq), quant_pre_bounded(v[1], rq),
-                                  quant_pre_bounded(v[2], rq), quant_pre_bounded(v[3], rq));
-        w[g / 4 + 1] = trunc_pack4_s8(quant_pre_bounded(v[4], rq), quant_pre_bounded(v[5], rq),
-                                      quant_pre_bounded(v[6], rq), quant_pre_bounded(v[7], rq));
+          for (int u = 0; u < 8; u += 2) {
+            const float2 d = add2(mul2(f2(__int2float_rn(int(r[g + u])), __int2float_rn(int(r[g + u + 1]))),
+                                       f2(p.mult, p.mult), k),
+                                  f2(b[g + u], b[g + u + 1]), k);
+            v[u] = d.x;
+            v[u + 1] = d.y;
+          }
+          gelu8_finite_x2(v, tt, k);
+          float2 q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[u] = quant_pre2(f2(v[2 * u], v[2 * u + 1]), rq, k);
+          w[g / 4] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
+          w[g / 4 + 1] = trunc_pack4_s8(q[2].x, q[2].y, q[3].x, q[3].y);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
+          gelu8(v, tt);
+          w[g / 4] = trunc_pack4_s8(quant_pre_bounded(v[0], rq), quant_pre_bounded(v[1], rq),
+                                    quant_pre_bounded(v[2], rq), quant_pre_bounded(v[3], rq));
+          w[g / 4 + 1] = trunc_pack4_s8(quant_pre_bounded(v[4], rq), quant_pre_bounded(v[5], rq),
+                                        quant_pre_bounded(v[6], rq), quant_pre_bounded(v[7], rq));
+        }
       }
       if (c.row < c.M) {
         uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);

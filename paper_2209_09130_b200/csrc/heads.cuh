@@ -7,9 +7,8 @@
 // (tests use a tolerance); tanh, exp and the softmax normaliser are numpy-exact.
 //
 // classify = two launches: pooler_kernel spreads the [B,H]x[H,H] pooler over
-// (32-column, 32-sequence) tiles — a warp owns 4 sequences, a lane one output column,
-// so every Wp row slice is one coalesced 128-byte load; classifier_kernel is one warp
-// per sequence (lanes over H, shuffle reduction) plus the exact softmax/argmax.
+// (32-column, 32-sequence, K-split) tiles with every weight load in flight at once;
+// classifier_kernel is one CTA per sequence (tanh, label dot products, softmax/argmax).
 #pragma once
 #include "numerics.cuh"
 
@@ -19,7 +18,8 @@ constexpr int HEAD_THREADS = 256;
 constexpr int HEAD_MAX_LABELS = 64;
 constexpr int POOL_COLS = 32;      // output columns per pooler CTA
 constexpr int POOL_SEQS = 32;      // sequences per pooler CTA
-constexpr int POOL_KSPLIT = 4;     // K quarters (grid.z)
+constexpr int POOL_KSPLIT = 8;     // K splits (grid.z)
+constexpr int POOL_MAX_KW = 16;    // K rows per warp: H / POOL_KSPLIT / 8 for H <= 1024
 
 struct HeadParams {
   const float* hidden;     // [T][H]
@@ -72,78 +72,127 @@ __device__ __forceinline__ void softmax_argmax(const float* lg, float* pr, int* 
   *label = best;
 }
 
-// pooler_kernel: CTA (x, y, z) = 32 output columns x up to 32 sequences x K-quarter z;
-// warp w reduces K rows [z*H/4 + w*H/32, ...) for all its sequences (lane = column, 32
-// independent accumulators); the 8 warp partials are added in a fixed order and written
-// to pooled[z][s][j].  classifier_kernel (one warp per sequence) adds the 4 quarters in
-// order, applies bias + numpy tanh, then the classifier dot products + exact softmax.
+// pooler_kernel: CTA (x, y, z) = 32 output columns x up to 32 sequences x K-split z (of
+// POOL_KSPLIT).  The CTA stages its [CLS] slices transposed in smem (hs[k][s]); warp w
+// owns H/POOL_KSPLIT/8 K rows and issues all of its Wp loads (lane = column, one
+// coalesced 128-byte row slice each) before any FMA, so the kernel is one memory round
+// trip plus register FMAs; the 8 warp partials are summed in a fixed order into
+// pooled[z][s][j].
 static __global__ void __launch_bounds__(HEAD_THREADS) pooler_kernel(const HeadParams p) {
-  extern __shared__ float sh[];           // h [POOL_SEQS][H/4] then partials [8][POOL_SEQS][32]
+  extern __shared__ float sh[];           // hs [KQ][32] then partials [8][32 seqs][32 cols]
   pdl_trigger();
   pdl_wait();
-  const int H = p.hidden_size, KQ = H / POOL_KSPLIT;
+  const int H = p.hidden_size, KQ = H / POOL_KSPLIT, kw = KQ / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * POOL_COLS + lane;
   const int s0 = blockIdx.y * POOL_SEQS;
   const int k_base = blockIdx.z * KQ;
   const int ns = min(POOL_SEQS, p.nseq - s0);
   float* hs = sh;
-  float* part = sh + POOL_SEQS * KQ;
-  for (int s = warp; s < ns; s += HEAD_THREADS / 32) {      // [CLS] row slices
-    const float* src = p.hidden + size_t(p.seq_start[s0 + s]) * H + k_base;
-    for (int k = lane; k < KQ; k += 32) hs[s * KQ + k] = src[k];
+  float* part = sh + KQ * POOL_SEQS;
+  float wv[POOL_MAX_KW];
+#pragma unroll
+  for (int i = 0; i < POOL_MAX_KW; ++i)
+    wv[i] = i < kw ? __ldg(p.pool_w + size_t(k_base + warp * kw + i) * H + j) : 0.0f;
+  for (int idx = threadIdx.x; idx < POOL_SEQS * KQ; idx += HEAD_THREADS) {
+    const int s = idx / KQ, k = idx - s * KQ;
+    hs[k * POOL_SEQS + s] = s < ns ? p.hidden[size_t(p.seq_start[s0 + s]) * H + k_base + k] : 0.0f;
   }
   __syncthreads();
   float acc[POOL_SEQS];
 #pragma unroll
   for (int s = 0; s < POOL_SEQS; ++s) acc[s] = 0.0f;
-  const int k_per = KQ / (HEAD_THREADS / 32);
-  const int k0 = warp * k_per;
-  if (j < H) {
-#pragma unroll 4
-    for (int k = k0; k < k0 + k_per; ++k) {
-      const float wk = __ldg(p.pool_w + size_t(k_base + k) * H + j);
 #pragma unroll
-      for (int s = 0; s < POOL_SEQS; ++s) acc[s] = __fmaf_rn(hs[s * KQ + k], wk, acc[s]);
+  for (int i = 0; i < POOL_MAX_KW; ++i) {
+    if (i < kw) {
+      const float4* h4 = reinterpret_cast<const float4*>(hs + (warp * kw + i) * POOL_SEQS);
+#pragma unroll
+      for (int q = 0; q < POOL_SEQS / 4; ++q) {
+        const float4 hv = h4[q];
+        acc[4 * q] = __fmaf_rn(hv.x, wv[i], acc[4 * q]);
+        acc[4 * q + 1] = __fmaf_rn(hv.y, wv[i], acc[4 * q + 1]);
+        acc[4 * q + 2] = __fmaf_rn(hv.z, wv[i], acc[4 * q + 2]);
+        acc[4 * q + 3] = __fmaf_rn(hv.w, wv[i], acc[4 * q + 3]);
+      }
     }
   }
 #pragma unroll
   for (int s = 0; s < POOL_SEQS; ++s) part[(warp * POOL_SEQS + s) * 32 + lane] = acc[s];
   __syncthreads();
   for (int s = warp; s < ns; s += HEAD_THREADS / 32) {
-    if (j >= H) continue;
     float v = 0.0f;
+#pragma unroll
     for (int w = 0; w < HEAD_THREADS / 32; ++w) v = __fadd_rn(v, part[(w * POOL_SEQS + s) * 32 + lane]);
     p.pooled[(size_t(blockIdx.z) * p.nseq + s0 + s) * H + j] = v;
   }
 }
 
+// classifier_kernel: one CTA per sequence.  Thread t owns columns t, t+256, ...: it adds
+// the POOL_KSPLIT partials in order, + bias, numpy tanh -> smem; each label's dot product
+// is a per-thread partial, a warp shuffle tree and a fixed-order sum of the 8 warp
+// results; thread 0 runs the exact softmax / argmax.
 static __global__ void __launch_bounds__(HEAD_THREADS) classifier_kernel(const HeadParams p) {
-  extern __shared__ float pooled_s[];     // [8 warps][H]
+  extern __shared__ float pooled_s[];     // [H] then red [8][HEAD_MAX_LABELS] then lg [HEAD_MAX_LABELS]
   __shared__ TanhTable tt;
   const int H = p.hidden_size, L = p.num_labels;
   load_tanh_table(&tt, threadIdx.x, HEAD_THREADS);
   pdl_trigger();
   pdl_wait();
-  __syncthreads();
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int s = blockIdx.x * (HEAD_THREADS / 32) + warp;
-  if (s >= p.nseq) return;
-  float* x = pooled_s + warp * H;
-  for (int k = lane; k < H; k += 32) {
-    float v = p.pooled[size_t(s) * H + k];
-    for (int z = 1; z < POOL_KSPLIT; ++z) v = __fadd_rn(v, p.pooled[(size_t(z) * p.nseq + s) * H + k]);
-    x[k] = np_tanhf(__fadd_rn(v, p.pool_b[k]), &tt);
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* x = pooled_s;
+  float* red = pooled_s + H;
+  float* lg = red + 8 * HEAD_MAX_LABELS;
+  float v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = threadIdx.x + i * HEAD_THREADS;
+    v[i] = 0.0f;
+    if (k < H) {
+      float parts[POOL_KSPLIT];
+#pragma unroll
+      for (int z = 0; z < POOL_KSPLIT; ++z) parts[z] = p.pooled[(size_t(z) * p.nseq + s) * H + k];
+      float a = parts[0];
+#pragma unroll
+      for (int z = 1; z < POOL_KSPLIT; ++z) a = __fadd_rn(a, parts[z]);
+      v[i] = a;
+    }
   }
-  __syncwarp();
-  float lg[HEAD_MAX_LABELS];
-  for (int l = 0; l < L; ++l) lg[l] = __fadd_rn(warp_dot(x, p.head_wt + size_t(l) * H, H), p.head_b[l]);
-  if (lane == 0) {
-    float pr[HEAD_MAX_LABELS];
+  __syncthreads();   // tanh table
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = threadIdx.x + i * HEAD_THREADS;
+    if (k < H) {
+      v[i] = np_tanhf(__fadd_rn(v[i], p.pool_b[k]), &tt);
+      x[k] = v[i];
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    float a = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = threadIdx.x + i * HEAD_THREADS;
+      if (k < H) a = __fmaf_rn(v[i], __ldg(p.head_wt + size_t(l) * H + k), a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0) red[warp * HEAD_MAX_LABELS + l] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < L) {
+    float a = 0.0f;
+#pragma unroll
+    for (int w = 0; w < HEAD_THREADS / 32; ++w) a = __fadd_rn(a, red[w * HEAD_MAX_LABELS + threadIdx.x]);
+    lg[threadIdx.x] = __fadd_rn(a, p.head_b[threadIdx.x]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float l2[HEAD_MAX_LABELS], pr[HEAD_MAX_LABELS];
+    for (int l = 0; l < L; ++l) l2[l] = lg[l];
     int lab;
-    softmax_argmax(lg, pr, &lab, L);
+    softmax_argmax(l2, pr, &lab, L);
     for (int l = 0; l < L; ++l) {
-      p.logits[size_t(s) * L + l] = lg[l];
+      p.logits[size_t(s) * L + l] = l2[l];
       p.probs[size_t(s) * L + l] = pr[l];
     }
     p.labels[s] = lab;

@@ -33,20 +33,12 @@ cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_classify(const HeadParams& p, cudaStream_t st) {
-  static thread_local int configured = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured != dev) {
-    cudaError_t e = cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = dev;
-  }
   const dim3 grid((p.hidden_size + POOL_COLS - 1) / POOL_COLS, (p.nseq + POOL_SEQS - 1) / POOL_SEQS, POOL_KSPLIT);
   const size_t smem = (size_t(POOL_SEQS) * p.hidden_size / POOL_KSPLIT + 8 * POOL_SEQS * 32) * sizeof(float);
   cudaError_t e = launch_ex(pooler_kernel, grid, dim3(HEAD_THREADS), smem, st, 1, p);
   if (e != cudaSuccess) return e;
-  return launch_ex(classifier_kernel, dim3((p.nseq + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32)), dim3(HEAD_THREADS),
-                   size_t(HEAD_THREADS / 32) * p.hidden_size * sizeof(float), st, 1, p);
+  return launch_ex(classifier_kernel, dim3(p.nseq), dim3(HEAD_THREADS),
+                   (size_t(p.hidden_size) + 9 * HEAD_MAX_LABELS) * sizeof(float), st, 1, p);
 }
 
 cudaError_t launch_tag(const HeadParams& p, cudaStream_t st) {

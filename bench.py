@@ -37,6 +37,27 @@ sys.path.insert(0, ROOT)
 
 MODEL = "bert-base"
 BATCH, SEQ = 32, 128
+
+
+class Workload:
+    """One BASELINE.json config as a bench workload.  The driver's default is c2
+    (configs[1]); c4 / c5 are the other throughput configs, selectable with --workload
+    (their scales come from on-device calibration, 8 rng(1) sequences)."""
+
+    def __init__(self, key, desc, model, task, labels, batch, seq, mode, pairs=False, strong=False):
+        self.key, self.desc, self.model, self.task, self.labels = key, desc, model, task, labels
+        self.batch, self.seq, self.mode, self.pairs, self.strong = batch, seq, mode, pairs, strong
+
+
+WORKLOADS = {
+    "c2": Workload("c2", "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 per GPU (configs[1])",
+                   "bert-base", "classification", 2, 32, 128, "FULLY_QUANT"),
+    "c4": Workload("c4", "BERT-large NER tag head, MHA-FFN INT8 24/24, batch 64 x seq 256 sharded over the GPUs "
+                   "(configs[3])", "bert-large", "sequence_labeling", 9, 64, 256, "FULLY_QUANT", strong=True),
+    "c5": Workload("c5", "BERT-base text-matching pairs, FFN-only INT8 12/12, batch 4096 x seq 64 sharded over "
+                   "the GPUs (configs[4])", "bert-base", "text_matching", 2, 4096, 64, "FFN_ONLY",
+                   pairs=True, strong=True),
+}
 METRIC = "BERT-base seq128 sentences/s (1/2/4/8 B200) & batch-1 p50 latency per mode"
 CALIB = os.path.join(ROOT, "tests", "golden", f"bench_calibration_{MODEL}.json")
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -50,11 +71,14 @@ def dist_env():
     return world, rank, local
 
 
-def build_model():
+def build_model(wl=None):
     from paper_2209_09130_b200.quantization import CalibrationTable
     from paper_2209_09130_b200.synthetic import bert_archive
 
-    arch = bert_archive(MODEL, task="classification", num_labels=2, seed=0, weight_scale=0.02)
+    wl = wl or WORKLOADS["c2"]
+    arch = bert_archive(wl.model, task=wl.task, num_labels=wl.labels, seed=0, weight_scale=0.02)
+    if wl.key != "c2":
+        return arch          # calibrated on the device by the caller
     with open(CALIB) as fh:
         table = CalibrationTable.from_json(fh.read())
     if table.model_fingerprint != arch.fingerprint:
@@ -63,11 +87,17 @@ def build_model():
     return arch
 
 
-def synthetic_batch(rank: int, batch: int = BATCH, seq: int = SEQ):
-    """cli._random_inputs recipe (reference cli.py:333-341): default_rng ids, segment 0, no padding."""
+def synthetic_batch(rank: int, batch: int = BATCH, seq: int = SEQ, pairs: bool = False):
+    """cli._random_inputs recipe (reference cli.py:333-341): default_rng ids, segment 0, no padding.
+    pairs: [CLS] a [SEP] b [SEP] with segment 1 after the first [SEP]."""
     rng = np.random.default_rng(rank)
-    ids = rng.integers(0, 30522, size=(batch, seq)).astype(np.int32).reshape(-1)
-    segs = np.zeros(batch * seq, np.int32)
+    ids = rng.integers(0, 30522, size=(batch, seq)).astype(np.int32)
+    segs = np.zeros((batch, seq), np.int32)
+    if pairs:
+        la = (seq - 3 + 1) // 2
+        ids[:, 0], ids[:, la + 1], ids[:, seq - 1] = 0, 1, 1      # [CLS]=0, [SEP]=1 (vocab order)
+        segs[:, la + 2:] = 1
+    ids, segs = ids.reshape(-1), segs.reshape(-1)
     seq_start = (np.arange(batch + 1) * seq).astype(np.int32)
     att = np.full(batch, seq, np.int32)
     return seq_start, att, ids, segs
@@ -146,23 +176,37 @@ def run_samp(args):
 
     from paper_2209_09130_b200 import _lib
     from paper_2209_09130_b200.engine import HEAD_CLASSIFY, IO_DEVICE, Engine
+    from paper_2209_09130_b200.engine import HEAD_TAG
     from paper_2209_09130_b200.plan import PrecisionPlan
 
-    arch = build_model()
+    wl = WORKLOADS[args.workload]
+    BATCH, SEQ = (wl.batch // world if wl.strong else wl.batch), wl.seq
+    if wl.strong and wl.batch % world:
+        raise SystemExit(f"--workload {wl.key}: batch {wl.batch} does not split over {world} GPUs")
+    arch = build_model(wl)
     eng = Engine(arch, device=local)
     L = arch.manifest.num_layers
-    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
-    seq_start, att, ids, segs = synthetic_batch(rank)
+    if arch.calibration is None:
+        from paper_2209_09130_b200.tokenization import EncodedInput
+        c_start, _, c_ids, c_segs = synthetic_batch(1, 8, SEQ, wl.pairs)
+        arch.calibration = eng.calibrate([EncodedInput(c_ids[c_start[i]:c_start[i + 1]].tolist(),
+                                                       c_segs[c_start[i]:c_start[i + 1]].tolist(), SEQ)
+                                          for i in range(8)])
+        eng._push_calibration()
+    plan = PrecisionPlan.prefix(wl.mode, L, L)
+    head_kind = HEAD_TAG if wl.task == "sequence_labeling" else HEAD_CLASSIFY
+    seq_start, att, ids, segs = synthetic_batch(rank, BATCH, SEQ, wl.pairs)
     T = int(seq_start[-1])
     d_ids = torch.from_numpy(ids).to(dev)
     d_segs = torch.from_numpy(segs).to(dev)
     nl = arch.manifest.num_labels
-    d_logits = torch.empty((BATCH, nl), dtype=torch.float32, device=dev)
+    rows = T if head_kind == HEAD_TAG else BATCH
+    d_logits = torch.empty((rows, nl), dtype=torch.float32, device=dev)
     d_probs = torch.empty_like(d_logits)
-    d_labels = torch.empty(BATCH, dtype=torch.int32, device=dev)
+    d_labels = torch.empty(rows, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     lib = _lib.load()
-    out = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), HEAD_CLASSIFY)
+    out = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), head_kind)
     codes = plan.codes()
     # a real (non-legacy) stream: the engine launches every kernel on it, so CUDA events
     # recorded on it bracket exactly the forward
@@ -230,7 +274,7 @@ def run_samp(args):
     e2e_ms = max_over_ranks(e2e_ms)
     e2e = {"value": world * BATCH * args.steps / (e2e_ms / 1e3), "unit": "sentences/s",
            "h2d_bytes_per_step": int(ids.nbytes + segs.nbytes),
-           "d2h_bytes_per_step": int(BATCH * nl * 4 * 2 + BATCH * 4)}
+           "d2h_bytes_per_step": int(rows * nl * 4 * 2 + rows * 4)}
 
     # ---------------- per-kernel device times (separate pass, CUDA events per launch)
     _lib.check(lib.samp_set_profiling(eng.handle, 1))
@@ -242,6 +286,7 @@ def run_samp(args):
     H, I = arch.manifest.hidden, arch.manifest.intermediate
     ops = gemm_ops(T, H, I)
     ops["attention_i8"] = 4 * BATCH * SEQ * SEQ * H
+    ops["attention_f16"] = 4 * BATCH * SEQ * SEQ * H
     kernels = {}
     for name, (tot_ms, n) in prof.items():
         avg = tot_ms / n
@@ -263,6 +308,9 @@ def run_samp(args):
     traffic = None
     if os.path.exists(TRAFFIC):
         traffic = json.load(open(TRAFFIC)).get(dom)
+    if dom.endswith("_f16"):
+        peak, peak_src = bf16, peak_src.replace("2 x ", "").replace(" (B200 dense int8 = 2 x dense bf16)", " (dense f16 = dense bf16)")
+        achieved = kernels[dom]["achieved_tops"]
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "ops_per_launch": ops[dom]}
@@ -271,8 +319,8 @@ def run_samp(args):
     clocks.__exit__(None, None, None)
     lat = {}
     b1_start, b1_att = np.array([0, SEQ], np.int32), np.array([SEQ], np.int32)
-    out1 = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), HEAD_CLASSIFY)
-    for label, mode, k in (("fp16", "FP", 0), ("ffn-only-12", "FFN_ONLY", L), ("fully-quant-12", "FULLY_QUANT", L)):
+    out1 = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), head_kind)
+    for label, mode, k in (("fp16", "FP", 0), (f"ffn-only-{L}", "FFN_ONLY", L), (f"fully-quant-{L}", "FULLY_QUANT", L)):
         pc = PrecisionPlan.prefix(mode, L, k).codes()
 
         def one(pc=pc):
@@ -290,16 +338,16 @@ def run_samp(args):
 
     line = None
     if rank == 0:
-        cpu = cpu_baseline(arch, plan, args) if (world == 1 and not args.no_cpu) else None
+        cpu = cpu_baseline(arch, plan, args, wl=wl) if (world == 1 and not args.no_cpu) else None
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "sentences/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic (random ids, random-init weights seed 0; reference-calibrated scales)",
-            "config": {"workload": "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 per GPU (configs[1])",
-                       "model": MODEL, "plan": "FULLY_QUANT k=12", "batch_per_gpu": BATCH, "seq_len": SEQ,
-                       "global_batch": BATCH * world, "parallelism": f"replicas x{world} (batch-sharded)",
-                       "l2": "flushed before every timed step (256 MiB write)"},
+            "config": {"workload": wl.desc, "model": wl.model, "plan": f"{wl.mode} k={L}", "batch_per_gpu": BATCH,
+                       "seq_len": SEQ, "global_batch": BATCH * world, "parallelism": f"replicas x{world} (batch-sharded)",
+                       "l2": "flushed before every timed step (256 MiB write)",
+                       "calibration": "reference (tests/golden)" if wl.key == "c2" else "on-device, 8 rng(1) sequences"},
             "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
             "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps,
             "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels,
@@ -320,14 +368,15 @@ def _blas_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(arch, plan, args, n_sent=None):
+def cpu_baseline(arch, plan, args, n_sent=None, wl=None):
     """The reference's CPU path (oracle port) on a bounded sample of the same workload."""
     from oracle import samp_oracle as orc
 
-    n_sent = n_sent or args.cpu_sentences
+    wl = wl or WORKLOADS["c2"]
+    n_sent = n_sent or (args.cpu_sentences if wl.key == "c2" else 2)
     amax = {s: e.amax for s, e in arch.calibration.entries.items()}
     model = orc.Model.from_manifest(arch.manifest, arch.tensors, amax)
-    seq_start, att, ids, segs = synthetic_batch(0)
+    seq_start, att, ids, segs = synthetic_batch(0, n_sent, wl.seq, wl.pairs)
     model.qlayer(0)  # weight quantization is load-time in the reference (cached), keep it out
     for i in range(arch.manifest.num_layers):
         model.qlayer(i)
@@ -335,10 +384,14 @@ def cpu_baseline(arch, plan, args, n_sent=None):
     for s in range(n_sent):
         r0, r1 = seq_start[s], seq_start[s + 1]
         h = orc.run(model, ids[r0:r1], segs[r0:r1], int(att[s]), plan.layer_precisions)
-        orc.classify_logits(model, h)
+        if wl.task == "sequence_labeling":
+            orc.tag_logits(model, h, int(att[s]))
+        else:
+            orc.classify_logits(model, h)
     dt = time.perf_counter() - t0
     return {"value": round(n_sent / dt, 4), "unit": "sentences/s", "cores": _blas_threads(), "kind": "port",
-            "sample": f"{n_sent} of the 32 x 128-token sentences, FULLY_QUANT 12/12 + classify head, "
+            "sample": f"{n_sent} of the {wl.batch} x {wl.seq}-token sentences, {wl.mode} "
+                      f"{arch.manifest.num_layers}/{arch.manifest.num_layers} + {wl.task} head, "
                       f"oracle port of the reference (numpy, OpenBLAS threads for the int8 GEMMs)"}
 
 
@@ -387,6 +440,8 @@ def main(argv=None):
     ap.add_argument("--cpu-sentences", type=int, default=12)
     ap.add_argument("--ref-sentences", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS),
+                    help="c2 = configs[1] (the driver's default); c4 / c5 = the other throughput configs")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

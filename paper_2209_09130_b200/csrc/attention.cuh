@@ -1,5 +1,8 @@
-// Padding-free (varlen) multi-head attention, one CTA per (128-query tile, head),
-// INT8 (kind::i8) or FP16 (kind::f16) operands.
+// Padding-free (varlen) multi-head attention, INT8 (kind::i8) or FP16 (kind::f16)
+// operands.  One CTA per (tile, head); a tile is either 128 queries of one sequence, or
+// several whole sequences of equal length S in {32, 64} packed block-diagonally (2 or 4
+// sequences share the 128 MMA rows; keys of the other sequences get P = 0 exactly, so
+// P.V over the packed keys equals each sequence's own product).
 //
 // INT8 semantics (reference pkg/src/samp/encoder.py:368-379, kernels.py:130-135):
 //   scores = F32(Q_q . K_q^T) * F32(s_q*s_k/sqrt(d)) + mask      mask = -10000 for keys >= att_len
@@ -9,18 +12,27 @@
 // FP semantics (encoder.py:298-305): scores = (Q.K^T)*F32(1/sqrt(d)) + mask, same softmax,
 //   ctx = P . V, with Q/K/V/P/ctx held in f16 (the reference's fp16-storage points).
 // Rows and keys of a sequence are its full (possibly padded) length S, so each sequence
-// sees exactly the reference's per-sequence arithmetic; packing sequences back to back
-// removes the reference's batch padding (cli.py:375-377 runs sequences one by one).
+// sees exactly the reference's per-sequence arithmetic.
 //
-// Data path: TMA loads Q [128 x d], K and V [S x d] straight out of the fused QKV
-// activation [T][3H] (64B swizzle for int8 rows of 64 B, 128B swizzle for f16 rows of
-// 128 B).  tcgen05.mma #1: S_acc[128 x S] = Q K^T into TMEM (K-major A and B).  The four
-// softmax warps own one query row per thread: they pull the row out of TMEM, write x and
-// e back into TMEM, reduce e with numpy's pairwise tree and store P into smem in the
-// 128B-swizzled K-major layout.  tcgen05.mma #2: O_acc[128 x 64] = P V, V consumed
-// MN-major straight from its TMA image.  P is produced in chunks of up to 256 keys so the
-// f16 path fits S = 512 in shared memory.
+// Data path: TMA loads Q [128 x d], K and V [keys x d] straight out of the fused QKV
+// activation [T][3H].  tcgen05.mma #1: S_acc[128 x keys] = Q K^T into TMEM.  Eight
+// softmax warps, two threads per query row (h = 0/1 take alternate 32-key chunks):
+//   pass 1  row max from the integer (INT8) / f32 (FP16) accumulators: x = RN(acc*m) is
+//           monotone in acc, so max/min of acc over the unmasked and the masked keys give
+//           the exact row max of x with one IMNMX per key;
+//   pass 2  e = numpy exp(x - max) -> TMEM.  When the row's exp arguments provably lie in
+//           [-86.5, 0] (checked per row from the pass-1 extremes; masked keys underflow to
+//           0) the exp runs on FFMA2 pairs with an exact exponent add instead of numpy's
+//           two-step scalef; otherwise the general scalar restatement runs;
+//   sum     numpy's pairwise tree over the row's S values of e (TMEM reads in order);
+//           S <= 128 is one leaf (h = 0), longer rows split at numpy's top-level split;
+//   pass 3  P = e / sum (quantized or f16) into the 128B-swizzled K-major A operand.
+// tcgen05.mma #2: O_acc[128 x 64] = P V, V consumed MN-major straight from its TMA image.
+// P is produced in chunks of up to 256 keys so the f16 path fits S = 512 in smem.
 #pragma once
+#include <climits>
+#include <type_traits>
+
 #include <cuda_fp16.h>
 
 #include "numerics.cuh"
@@ -29,14 +41,14 @@
 namespace samp {
 
 constexpr int ATT_THREADS = 288;   // warp 0: TMA + MMA + TMEM owner; warps 1-8: softmax (2 per row)
-constexpr int ATT_MAX_LEAVES = 8;  // numpy tree leaves for S <= 512
 constexpr int ATT_MAX_KEYS = 512;
 constexpr int ATT_P_CHUNK = 256;   // keys of P written per MMA-2 round
 
 struct AttnParams {
   void* ctx_out;              // [T][H] int8 codes (INT8) or f16 values (FP16)
-  const int* tile_seq;        // [ntiles] sequence of each 128-query tile
-  const int* tile_q0;         // [ntiles] first query (within the sequence)
+  const int* tile_seq;        // [ntiles] first sequence of each tile
+  const int* tile_q0;         // [ntiles] first query (within the sequence); 0 for packed tiles
+  const int* tile_cnt;        // [ntiles] sequences in the tile (> 1: equal S in {32, 64})
   const int* seq_start;       // [nseq+1] packed row offsets
   const int* att_len;         // [nseq]
   int hidden;                 // H
@@ -47,6 +59,7 @@ struct AttnParams {
   int tmem_cols;              // power of two >= max(64, padded keys in the batch)
   float* amax;                // FP16 calibration: site amax array (null = off)
   int site_sm, site_ctx;      // L.attn.softmax / L.attn.out_in
+  X2 k = x2_consts();         // opaque FFMA2 constants (numerics.cuh)
 };
 
 template <bool F16>
@@ -69,13 +82,99 @@ struct AttnLayout {
     v_off = k_off + kv;
     p_off = ((v_off + kv + 1023) / 1024) * 1024;
     x_off = p_off + 128 * pchunk * C::P_ELT;
-    bar_off = x_off + (2 + 2 * ATT_MAX_LEAVES) * 128 * 4;
+    bar_off = x_off + 6 * 128 * 4;
     total = bar_off + 64 + 1024;
   }
 };
 
 // named barrier among the 256 softmax threads
 __device__ __forceinline__ void att_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+constexpr float ATT_EXP_FAST_MIN = -86.5f;          // x - max >= this  =>  k >= -125 (normal result)
+constexpr float ATT_EXP_LO_CUT = -103.97208404541015625f;
+constexpr float ATT_MASK = -10000.0f;
+
+// np_expf_nonpos on a pair whose arguments lie in [ATT_EXP_FAST_MIN, 0]: the clamp and the
+// underflow select are unreachable and p * 2^k (k >= -125, p in [0.7, 1.42]) is normal, so
+// numpy's scalef reduces to an exact exponent add.  Every other operation is the scalar
+// restatement's (numerics.cuh np_expf) on FFMA2 lanes: bit-identical on that domain.
+__device__ __forceinline__ float2 np_exp2_fast(float2 d, const X2& k) {
+  const float2 kk0 = add2(mul2(d, f2(1.442695040888963407359924681001892137f, 1.442695040888963407359924681001892137f), k),
+                          f2(12582912.0f, 12582912.0f), k);
+  const int k0 = __float_as_int(kk0.x) - 0x4B400000, k1 = __float_as_int(kk0.y) - 0x4B400000;
+  const float2 kk = add2(kk0, f2(-12582912.0f, -12582912.0f), k);
+  float2 r = __ffma2_rn(kk, f2(-6.93145752e-1f, -6.93145752e-1f), d);
+  r = __ffma2_rn(kk, f2(-1.42860677e-6f, -1.42860677e-6f), r);
+  r = __ffma2_rn(kk, f2(0.0f, 0.0f), r);
+  float2 num = __ffma2_rn(f2(5.082762527590693718096e-04f, 5.082762527590693718096e-04f), r,
+                          f2(6.757896990527504603057e-03f, 6.757896990527504603057e-03f));
+  num = __ffma2_rn(num, r, f2(5.114512081637298353406e-02f, 5.114512081637298353406e-02f));
+  num = __ffma2_rn(num, r, f2(2.473615434895520810817e-01f, 2.473615434895520810817e-01f));
+  num = __ffma2_rn(num, r, f2(7.257664613233124478488e-01f, 7.257664613233124478488e-01f));
+  num = __ffma2_rn(num, r, f2(9.999999999980870924916e-01f, 9.999999999980870924916e-01f));
+  float2 den = __ffma2_rn(f2(2.159509375685829852307e-02f, 2.159509375685829852307e-02f), r,
+                          f2(-2.742335390411667452936e-01f, -2.742335390411667452936e-01f));
+  den = __ffma2_rn(den, r, f2(1.0f, 1.0f));
+  // make_recip(den) + div_fast(num, .) per lane
+  const float2 r0 = f2(rcp_approx_ftz(den.x), rcp_approx_ftz(den.y));
+  const float2 nden = f2(-den.x, -den.y);
+  const float2 rr = __ffma2_rn(r0, __ffma2_rn(nden, r0, f2(1.0f, 1.0f)), r0);
+  const float2 q = __ffma2_rn(num, rr, f2(k.pzero, k.pzero));
+  const float2 p = __ffma2_rn(rr, __ffma2_rn(nden, q, num), q);
+  return f2(__int_as_float(__float_as_int(p.x) + (k0 << 23)), __int_as_float(__float_as_int(p.y) + (k1 << 23)));
+}
+
+// accumulator -> float: INT8 accumulators satisfy |acc| <= 64*128*128 = 2^20, so
+// F32(acc) = (1.5*2^23 + acc) - 1.5*2^23 exactly (an integer add and a packed subtract)
+template <bool F16>
+__device__ __forceinline__ float2 acc_pair(uint32_t a, uint32_t b, const X2& k) {
+  if constexpr (F16) {
+    return f2(__uint_as_float(a), __uint_as_float(b));
+  } else {
+    return add2(f2(__int_as_float(0x4B400000 + int(a)), __int_as_float(0x4B400000 + int(b))),
+                f2(-12582912.0f, -12582912.0f), k);
+  }
+}
+
+// numpy leaf (n <= 128) over e values in TMEM columns [col, col + n) of this thread's
+// lane: 8 strided accumulators over the body, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the
+// n % 8 tail sequentially; n < 8: 0 + sequential.  col is a multiple of 8 and uniform
+// across the warp (tcgen05.ld is warp-collective).
+__device__ __forceinline__ float att_leaf(uint32_t ta, int col, int n, const X2& k) {
+  const int body = n - (n & 7);
+  float res = 0.0f;
+  if (body > 0) {
+    float2 r[4];
+    for (int g = 0; g < body; g += 32) {
+      uint32_t u[4][8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (g + 8 * i < body) tmem_ld8(ta + col + g + 8 * i, u[i]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (g + 8 * i < body) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 v = f2(__uint_as_float(u[i][2 * j]), __uint_as_float(u[i][2 * j + 1]));
+            r[j] = (g + i == 0) ? v : add2(r[j], v, k);
+          }
+        }
+      }
+    }
+    res = __fadd_rn(__fadd_rn(__fadd_rn(r[0].x, r[0].y), __fadd_rn(r[1].x, r[1].y)),
+                    __fadd_rn(__fadd_rn(r[2].x, r[2].y), __fadd_rn(r[3].x, r[3].y)));
+  }
+  if (n & 7) {
+    uint32_t u[8];
+    tmem_ld8(ta + col + body, u);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 7; ++j)
+      if (j < (n & 7)) res = __fadd_rn(res, __uint_as_float(u[j]));
+  }
+  return res;
+}
 
 template <bool F16>
 __global__ void __launch_bounds__(ATT_THREADS, 3)
@@ -88,17 +187,18 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
   const AttnLayout<F16> lay(keys_cap);
   uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
   uint64_t* bar_s = bar_load + 1;       // MMA-1 done
-  uint64_t* bar_p = bar_load + 2;       // P chunk written (128 arrivals per phase)
+  uint64_t* bar_p = bar_load + 2;       // P chunk written (256 arrivals per phase)
   uint64_t* bar_pf = bar_load + 3;      // MMA-2 round done (P buffer free / O ready)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_load + 4);
 
   const int tile = blockIdx.x, head = blockIdx.y;
   const int seq = p.tile_seq[tile];
   const int q0 = p.tile_q0[tile];
-  const int row0 = p.seq_start[seq];
-  const int S = p.seq_start[seq + 1] - row0;
-  const int att = p.att_len[seq];
-  const int nkp = (S + 31) & ~31;       // keys padded to the MMA K step (32 covers both kinds)
+  const int cnt = p.tile_cnt[tile];
+  const int krow0 = p.seq_start[seq];
+  const int S = p.seq_start[seq + 1] - krow0;          // every sequence of a packed tile has this length
+  const int nk = cnt * S;                               // keys of the tile
+  const int nkp = (nk + 31) & ~31;                      // padded to the MMA K step (32 covers both kinds)
   const int nchunks = (nkp + ATT_P_CHUNK - 1) / ATT_P_CHUNK;
   const uint32_t warp = warp_id();
 
@@ -122,11 +222,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
       mbar_expect_tx(bar_load, 128 * C::ROW_BYTES + 2 * nblk * 64 * C::ROW_BYTES);
       const int H = p.hidden;
       // one tensor map (box = one head row x 64 rows) serves Q, K and V
-      tma_load_2d(smem + lay.q_off, &map_qkv, head * 64, row0 + q0, bar_load);
-      tma_load_2d(smem + lay.q_off + 64 * C::ROW_BYTES, &map_qkv, head * 64, row0 + q0 + 64, bar_load);
+      tma_load_2d(smem + lay.q_off, &map_qkv, head * 64, krow0 + q0, bar_load);
+      tma_load_2d(smem + lay.q_off + 64 * C::ROW_BYTES, &map_qkv, head * 64, krow0 + q0 + 64, bar_load);
       for (int b = 0; b < nblk; ++b) {
-        tma_load_2d(smem + lay.k_off + b * 64 * C::ROW_BYTES, &map_qkv, H + head * 64, row0 + b * 64, bar_load);
-        tma_load_2d(smem + lay.v_off + b * 64 * C::ROW_BYTES, &map_qkv, 2 * H + head * 64, row0 + b * 64, bar_load);
+        tma_load_2d(smem + lay.k_off + b * 64 * C::ROW_BYTES, &map_qkv, H + head * 64, krow0 + b * 64, bar_load);
+        tma_load_2d(smem + lay.v_off + b * 64 * C::ROW_BYTES, &map_qkv, 2 * H + head * 64, krow0 + b * 64, bar_load);
       }
       mbar_wait(bar_load, 0);
       tc_fence_after();
@@ -164,163 +264,183 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     }
     __syncwarp();
   } else {
-    // two threads per query row: h = 0 (warps 1-4) and h = 1 (warps 5-8) of the same
-    // TMEM lane quarter.  Element-wise passes split the 32-column chunks between them;
-    // inside every numpy leaf h owns the strided accumulators r[4h..4h+3], and
-    // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) is exactly numpy's combine.
+    const X2 kx = p.k;
     const int quarter = warp & 3;
     const int h = int(warp - 1) >> 2;
     const int r = quarter * 32 + lane_id();            // query row within the tile
     const uint32_t ta = tmem + (uint32_t(quarter * 32) << 16);
-    float* xch = reinterpret_cast<float*>(smem + lay.x_off);   // [2][128] max / denom exchange
-    float* part = xch + 2 * 128;                               // [2][ATT_MAX_LEAVES][128]
+    int* ixch = reinterpret_cast<int*>(smem + lay.x_off);     // [3][2][128] pass-1 extremes
+    float* xch = reinterpret_cast<float*>(smem + lay.x_off);  // reused: [2][128] partial sums
+    // this row's sequence: packed tiles hold whole sequences of S rows (S % 32 == 0, so a
+    // warp's 32 rows never straddle two sequences: kbeg is warp-uniform)
+    const int sub = cnt > 1 ? min(r / S, cnt - 1) : 0;
+    const int kbeg = sub * S;
+    const int att = p.att_len[seq + sub];
+    const bool live = cnt > 1 ? r < nk : q0 + r < S;
+    const int nrow = (S + 31) & ~31;                   // this row's key chunks: [kbeg, kbeg + nrow)
+    const float m = p.mult_scores;
     mbar_wait(bar_s, 0);
     tc_fence_after();
 
-    // pass 1: x = acc*mult + mask -> TMEM, row max over the S real keys
-    // (chunks entirely inside [0, min(att, S)) skip the per-key mask / bounds checks)
-    float mx = -INFINITY;
-    const int clean = min(att, S);
-    for (int c0 = 32 * h; c0 < nkp; c0 += 64) {
+    // ---- pass 1: extremes of the accumulators over unmasked [0, att) and masked [att, S)
+    // (INT8: int32 order == order of x = RN(F32(acc)*m), m > 0; FP16: f32 order likewise)
+    using Acc = typename std::conditional<F16, float, int>::type;
+    auto as_acc = [](uint32_t u) -> Acc {
+      if constexpr (F16) return __uint_as_float(u); else return int(u);
+    };
+    Acc lowest, highest;
+    if constexpr (F16) { lowest = -INFINITY; highest = INFINITY; } else { lowest = INT_MIN; highest = INT_MAX; }
+    Acc umax = lowest, umin = highest, mmax = lowest;
+    for (int c0 = 32 * h; c0 < nrow; c0 += 64) {
       uint32_t v[32];
-      tmem_ld32(ta + c0, v);
+      tmem_ld32(ta + kbeg + c0, v);
       tmem_wait_ld();
-      if (c0 + 32 <= clean) {
+      if (c0 + 32 <= att) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float acc = F16 ? __uint_as_float(v[j]) : __int2float_rn(int(v[j]));
-          const float x = __fadd_rn(__fmul_rn(acc, p.mult_scores), 0.0f);
-          mx = fmaxf(mx, x);
-          v[j] = __float_as_uint(x);
+          umax = max(umax, as_acc(v[j]));
+          umin = min(umin, as_acc(v[j]));
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int key = c0 + j;
-          const float acc = F16 ? __uint_as_float(v[j]) : __int2float_rn(int(v[j]));
-          const float x = __fadd_rn(__fmul_rn(acc, p.mult_scores), key < att ? 0.0f : -10000.0f);
-          if (key < S) mx = fmaxf(mx, x);
-          v[j] = __float_as_uint(x);
+          const Acc a = as_acc(v[j]);
+          if (key < att) { umax = max(umax, a); umin = min(umin, a); }
+          else if (key < S) mmax = max(mmax, a);
         }
       }
-      tmem_st32(ta + c0, v);
     }
-    tmem_wait_st();
-    xch[h * 128 + r] = mx;
-    att_bar();
-    mx = fmaxf(xch[r], xch[128 + r]);
-    // pass 2: e = exp(x - max) -> TMEM (0 past S); x - max <= 0 (numpy exp on that domain)
-    for (int c0 = 32 * h; c0 < nkp; c0 += 64) {
+    {
+      Acc* ex = reinterpret_cast<Acc*>(ixch);
+      ex[(0 * 2 + h) * 128 + r] = umax;
+      ex[(1 * 2 + h) * 128 + r] = umin;
+      ex[(2 * 2 + h) * 128 + r] = mmax;
+      att_bar();
+      umax = max(ex[r], ex[128 + r]);
+      umin = min(ex[256 + r], ex[384 + r]);
+      mmax = max(ex[512 + r], ex[640 + r]);
+    }
+    auto xval = [&](Acc a) -> float {
+      if constexpr (F16) return __fmul_rn(a, m); else return __fmul_rn(__int2float_rn(a), m);
+    };
+    const bool has_u = att > 0, has_m = att < S;
+    const float xm = has_m ? __fadd_rn(xval(mmax), ATT_MASK) : -INFINITY;
+    const float mx = has_u ? fmaxf(xval(umax), xm) : xm;
+    // fast exp for this row: every unmasked argument in [-86.5, 0], every masked one <= lo_cut
+    const bool fast_row = !live || ((!has_u || __fsub_rn(xval(umin), mx) >= ATT_EXP_FAST_MIN) &&
+                                    (!has_m || __fsub_rn(xm, mx) <= ATT_EXP_LO_CUT));
+    const bool fast = __all_sync(0xffffffffu, fast_row);
+    const float2 negmx = f2(-mx, -mx), mm = f2(m, m);
+
+    // ---- pass 2: e = exp(x - max) -> TMEM (0 past S)
+    for (int c0 = 32 * h; c0 < nrow; c0 += 64) {
       uint32_t v[32];
-      tmem_ld32(ta + c0, v);
+      tmem_ld32(ta + kbeg + c0, v);
       tmem_wait_ld();
-      if (c0 + 32 <= S) {
+      if (fast) {
+        const bool clean = c0 + 32 <= att;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(np_expf_nonpos(__fsub_rn(__uint_as_float(v[j]), mx)));
+        for (int j = 0; j < 32; j += 2) {
+          const float2 x = mul2(acc_pair<F16>(v[j], v[j + 1], kx), mm, kx);
+          const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
+          v[j] = __float_as_uint(clean || c0 + j < att ? e.x : 0.0f);
+          v[j + 1] = __float_as_uint(clean || c0 + j + 1 < att ? e.y : 0.0f);
+        }
       } else {
-#pragma unroll
+#pragma unroll 4
         for (int j = 0; j < 32; ++j) {
-          const float e = (c0 + j) < S ? np_expf_nonpos(__fsub_rn(__uint_as_float(v[j]), mx)) : 0.0f;
-          v[j] = __float_as_uint(e);
+          const int key = c0 + j;
+          float x = xval(as_acc(v[j]));
+          if (key >= att) x = __fadd_rn(x, ATT_MASK);
+          v[j] = __float_as_uint(key < S ? np_expf_nonpos(__fsub_rn(x, mx)) : 0.0f);
         }
       }
-      tmem_st32(ta + c0, v);
+      tmem_st32(ta + kbeg + c0, v);
     }
     tmem_wait_st();
     tc_fence_before();
     att_bar();                                    // every e of the row is in TMEM
     tc_fence_after();
-    // numpy pairwise sum over the S keys: half-leaf partials first ...
-    auto half_leaf = [&](int lo, int n, int li) {
-      if (n >= 8) {
-        const int body = n - (n & 7);
-        float acc[4];
-        uint32_t u[8];
-        tmem_ld8(ta + lo, u);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] = __uint_as_float(u[4 * h + j]);
-        for (int i = 8; i < body; i += 8) {
-          tmem_ld8(ta + lo + i, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] = __fadd_rn(acc[j], __uint_as_float(u[4 * h + j]));
-        }
-        part[(h * ATT_MAX_LEAVES + li) * 128 + r] = __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
-      }
-      return 0.0f;
-    };
-    pw_tree_eval(S, half_leaf);
-    att_bar();
-    // ... then h = 0 combines leaves (+ sequential tails) up numpy's tree
-    if (h == 0) {
-      auto full_leaf = [&](int lo, int n, int li) {
-        float res = 0.0f;
-        int tail_lo = lo;
-        if (n >= 8) {
-          res = __fadd_rn(part[li * 128 + r], part[(ATT_MAX_LEAVES + li) * 128 + r]);
-          tail_lo = lo + n - (n & 7);
-        }
-        uint32_t u[8];
-        if (tail_lo < lo + n) {
-          tmem_ld8(ta + tail_lo, u);
-          tmem_wait_ld();
-          for (int j = 0; j < lo + n - tail_lo; ++j) res = __fadd_rn(res, __uint_as_float(u[j]));
-        }
-        return res;
-      };
-      xch[r] = __fadd_rn(0.0f, pw_tree_eval(S, full_leaf));
+
+    // ---- numpy pairwise sum over the row's S values (np.sum = 0 + tree)
+    float part = 0.0f;
+    if (S <= 128) {
+      if (h == 0) part = att_leaf(ta, kbeg, S, kx);
+    } else {                                      // single-sequence tile, kbeg = 0
+      const int n2 = pw_split(S);
+      const int lo = h ? n2 : 0, n = h ? S - n2 : n2;
+      auto leaf = [&](int l, int ln, int) { return att_leaf(ta, lo + l, ln, kx); };
+      part = pw_tree_eval(n, leaf);
     }
+    xch[h * 128 + r] = part;
     att_bar();
-    const float denom = xch[r];
+    const float denom = S <= 128 ? __fadd_rn(0.0f, xch[r]) : __fadd_rn(0.0f, __fadd_rn(xch[r], xch[128 + r]));
     // denom in [1, S] and e in [0, 1]: the hoisted-reciprocal quotient is exact (numerics.cuh)
     const Recip rden = make_recip(denom), rsm = make_recip(F16 ? 1.0f : p.s_softmax);
-    // pass 3: P = e / sum (quantized or f16) into the 128B-swizzled K-major A operand
+
+    // ---- pass 3: P = e / sum (quantized or f16) into the 128B-swizzled K-major A operand
     uint8_t* prow = smem + lay.p_off + r * 128;
-    const bool row_live = q0 + r < S;
+    auto pstore = [&](int local, const uint32_t (&w)[16]) {   // 32 keys at chunk-local column `local`
+      uint8_t* base = prow + (local / C::KEYS_PER_PBLK) * 16384;
+      const int chunk0 = ((local % C::KEYS_PER_PBLK) * C::P_ELT) >> 4;
+#pragma unroll
+      for (int u = 0; u < 2 * C::P_ELT; ++u)
+        *reinterpret_cast<uint4*>(base + (((chunk0 + u) ^ (r & 7)) << 4)) =
+            make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+    };
     float amx_sm = 0.0f;
+    const float2 rden_r = f2(rden.r, rden.r), rden_ns = f2(-rden.s, -rden.s);
+    const float2 rsm_r = f2(rsm.r, rsm.r), rsm_ns = f2(-rsm.s, -rsm.s);
+    auto div_pair = [&](float2 x, float2 rr, float2 ns) {       // div_fast on a pair
+      const float2 q = __ffma2_rn(x, rr, f2(kx.pzero, kx.pzero));
+      return __ffma2_rn(rr, __ffma2_rn(ns, q, x), q);
+    };
     for (int ch = 0; ch < nchunks; ++ch) {
       if (ch > 0) mbar_wait(bar_pf, (ch - 1) & 1);    // previous round consumed the buffer
       const int k_lo = ch * ATT_P_CHUNK, k_hi = min(nkp, k_lo + ATT_P_CHUNK);
       for (int c0 = k_lo + 32 * h; c0 < k_hi; c0 += 64) {
-        uint32_t v[32];
-        tmem_ld32(ta + c0, v);
-        tmem_wait_ld();
-        uint32_t w[16];
-        if constexpr (F16) {
+        uint32_t w[16] = {};
+        const int key0 = c0 - kbeg;                   // sequence-local key of the chunk
+        if (key0 >= 0 && key0 < nrow) {               // warp-uniform: the row's own keys
+          uint32_t v[32];
+          tmem_ld32(ta + c0, v);
+          tmem_wait_ld();
+          if constexpr (F16) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float a = (c0 + j) < S ? div_fast(__uint_as_float(v[j]), rden) : 0.0f;
-            const float b = (c0 + j + 1) < S ? div_fast(__uint_as_float(v[j + 1]), rden) : 0.0f;
-            if (row_live) amx_sm = fmaxf(amx_sm, fmaxf(a, b));
-            __half2 hv = __floats2half2_rn(a, b);
-            w[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
-          }
-        } else {
+            for (int j = 0; j < 32; j += 2) {
+              const float2 pv = div_pair(f2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), rden_r, rden_ns);
+              const float a = key0 + j < S ? pv.x : 0.0f;
+              const float b = key0 + j + 1 < S ? pv.y : 0.0f;
+              if (live) amx_sm = fmaxf(amx_sm, fmaxf(a, b));
+              __half2 hv = __floats2half2_rn(a, b);
+              w[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+          } else {
+            // probabilities are >= +0, so quantize's copysign(0.5, y) is +0.5
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float q[4];
+            for (int j = 0; j < 32; j += 4) {
+              float2 q[2];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              q[u] = (c0 + j + u) < S ? quant_pre_bounded(div_fast(__uint_as_float(v[j + u]), rden), rsm) : 0.0f;
-            w[j / 4] = trunc_pack4_s8(q[0], q[1], q[2], q[3]);
+              for (int u = 0; u < 2; ++u) {
+                const float2 pv = div_pair(f2(__uint_as_float(v[j + 2 * u]), __uint_as_float(v[j + 2 * u + 1])),
+                                           rden_r, rden_ns);
+                q[u] = add2(div_pair(pv, rsm_r, rsm_ns), f2(0.5f, 0.5f), kx);
+                q[u].x = key0 + j + 2 * u < S ? q[u].x : 0.0f;
+                q[u].y = key0 + j + 2 * u + 1 < S ? q[u].y : 0.0f;
+              }
+              w[j / 4] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
+            }
           }
         }
-        // 32 keys = 32 (int8) or 64 (f16) bytes: 2 or 4 swizzled 16-byte chunks
-        const int local = c0 - k_lo;
-        uint8_t* base = prow + (local / C::KEYS_PER_PBLK) * 16384;
-        const int chunk0 = ((local % C::KEYS_PER_PBLK) * C::P_ELT) >> 4;
-#pragma unroll
-        for (int u = 0; u < 2 * C::P_ELT; ++u)
-          *reinterpret_cast<uint4*>(base + (((chunk0 + u) ^ (r & 7)) << 4)) =
-              make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+        pstore(c0 - k_lo, w);                         // other sequences' keys: P = 0
       }
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(bar_p);
     }
 
-    // context rows of this sequence: h writes output columns [32h, 32h+32)
+    // context rows: h writes output columns [32h, 32h+32)
     mbar_wait(bar_pf, (nchunks - 1) & 1);
     tc_fence_after();
     uint32_t o[32];
@@ -328,9 +448,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     tmem_wait_ld();
     const Recip rctx = make_recip(F16 ? 1.0f : p.s_ctx);
     float amx_ctx = 0.0f;
-    if (q0 + r < S) {
+    if (live) {
+      const size_t orow = size_t(krow0 + q0 + r);
       if constexpr (F16) {
-        __half* dst = static_cast<__half*>(p.ctx_out) + size_t(row0 + q0 + r) * p.hidden + head * 64 + 32 * h;
+        __half* dst = static_cast<__half*>(p.ctx_out) + orow * p.hidden + head * 64 + 32 * h;
         uint32_t w[16];
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
@@ -345,7 +466,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
           for (int j = 0; j < 32; ++j) amx_ctx = fmaxf(amx_ctx, fabsf(__uint_as_float(o[j])));
         }
       } else {
-        int8_t* dst = static_cast<int8_t*>(p.ctx_out) + size_t(row0 + q0 + r) * p.hidden + head * 64 + 32 * h;
+        int8_t* dst = static_cast<int8_t*>(p.ctx_out) + orow * p.hidden + head * 64 + 32 * h;
         uint32_t w[8];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {

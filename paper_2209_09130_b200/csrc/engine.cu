@@ -122,9 +122,9 @@ struct Activations {
 };
 
 struct Geometry {
-  std::vector<int> seq_start, att_len, tile_seq, tile_q0;
+  std::vector<int> seq_start, att_len, tile_seq, tile_q0, tile_cnt;
   int nseq = 0, T = 0, ntiles = 0, max_nkp = 0;
-  int *d_seq_start = nullptr, *d_att_len = nullptr, *d_tile_seq = nullptr, *d_tile_q0 = nullptr;
+  int *d_seq_start = nullptr, *d_att_len = nullptr, *d_tile_seq = nullptr, *d_tile_q0 = nullptr, *d_tile_cnt = nullptr;
   int cap_seq = 0, cap_tiles = 0;
 };
 
@@ -244,15 +244,33 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
   g.tile_q0.clear();
   g.max_nkp = 0;
   e->h_pos.resize(seq_start[nseq]);
+  g.tile_cnt.clear();
   for (int s = 0; s < nseq; ++s) {
     const int S = seq_start[s + 1] - seq_start[s];
     g.att_len[s] = std::min(att_len[s], S);
-    for (int q = 0; q < S; q += 128) {
-      g.tile_seq.push_back(s);
-      g.tile_q0.push_back(q);
-    }
     for (int t = 0; t < S; ++t) e->h_pos[seq_start[s] + t] = t;
-    g.max_nkp = std::max(g.max_nkp, (S + 31) & ~31);
+  }
+  // attention tiles: 128 queries of one sequence, or up to 128/S consecutive sequences of
+  // equal length S in {32, 64} packed block-diagonally into one tile (attention.cuh)
+  for (int s = 0; s < nseq;) {
+    const int S = seq_start[s + 1] - seq_start[s];
+    int cnt = 1;
+    if (S == 32 || S == 64) {
+      while (cnt < 128 / S && s + cnt < nseq && seq_start[s + cnt + 1] - seq_start[s + cnt] == S) ++cnt;
+    }
+    if (cnt > 1) {
+      g.tile_seq.push_back(s);
+      g.tile_q0.push_back(0);
+      g.tile_cnt.push_back(cnt);
+    } else {
+      for (int q = 0; q < S; q += 128) {
+        g.tile_seq.push_back(s);
+        g.tile_q0.push_back(q);
+        g.tile_cnt.push_back(1);
+      }
+    }
+    g.max_nkp = std::max(g.max_nkp, (cnt * S + 31) & ~31);
+    s += cnt;
   }
   g.T = seq_start[nseq];
   g.ntiles = int(g.tile_seq.size());
@@ -263,16 +281,18 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
     g.d_att_len = e->mem.alloc<int>(g.cap_seq);
   }
   if (g.ntiles > g.cap_tiles) {
-    if (g.d_tile_seq) { e->mem.release(g.d_tile_seq); e->mem.release(g.d_tile_q0); }
+    if (g.d_tile_seq) { e->mem.release(g.d_tile_seq); e->mem.release(g.d_tile_q0); e->mem.release(g.d_tile_cnt); }
     g.cap_tiles = std::max(g.ntiles, 64);
     g.d_tile_seq = e->mem.alloc<int>(g.cap_tiles);
     g.d_tile_q0 = e->mem.alloc<int>(g.cap_tiles);
+    g.d_tile_cnt = e->mem.alloc<int>(g.cap_tiles);
   }
   ensure_activations(e, g.T);
   SAMP_CUDA(cudaMemcpyAsync(g.d_seq_start, g.seq_start.data(), (nseq + 1) * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(g.d_att_len, g.att_len.data(), nseq * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(g.d_tile_seq, g.tile_seq.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(g.d_tile_q0, g.tile_q0.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaMemcpyAsync(g.d_tile_cnt, g.tile_cnt.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(e->act.pos, e->h_pos.data(), g.T * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));  // host vectors may change on the next call
 }
@@ -404,6 +424,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.ctx_out = a.ctx_i8;
     ap.tile_seq = e->geo.d_tile_seq;
     ap.tile_q0 = e->geo.d_tile_q0;
+    ap.tile_cnt = e->geo.d_tile_cnt;
     ap.seq_start = e->geo.d_seq_start;
     ap.att_len = e->geo.d_att_len;
     ap.hidden = H;
@@ -444,6 +465,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.ctx_out = a.ctx_f16;
     ap.tile_seq = e->geo.d_tile_seq;
     ap.tile_q0 = e->geo.d_tile_q0;
+    ap.tile_cnt = e->geo.d_tile_cnt;
     ap.seq_start = e->geo.d_seq_start;
     ap.att_len = e->geo.d_att_len;
     ap.hidden = H;

@@ -43,13 +43,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_addr(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread is parked until the phase
+// completes (or the hint expires) instead of re-issuing try_wait every few cycles,
+// which would steal issue slots from the warps doing the work on the same SM sub-partition
+#ifndef SAMP_MBAR_HINT_NS
+#define SAMP_MBAR_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SAMP_MBAR_HINT_NS > 0
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      " @!P1 bra WAIT_%=;\n}\n"
+      :: "r"(smem_addr(bar)), "r"(parity), "r"(SAMP_MBAR_HINT_NS) : "memory");
+#else
   asm volatile(
       "{\n .reg .pred P1;\n"
       "WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       " @!P1 bra WAIT_%=;\n}\n"
       :: "r"(smem_addr(bar)), "r"(parity) : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ PDL

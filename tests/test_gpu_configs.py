@@ -206,3 +206,25 @@ def test_c3_sweep_grid_varlen(request):
                     np.testing.assert_array_equal(batch.sequence(s), want, err_msg=f"S={lens[s]}")
                 else:
                     _fp16_close(batch.sequence(s), want, f"{mode} k={k} S={lens[s]}")
+
+
+# ---------------------------------------------------------------- packed attention tiles
+def test_packed_short_sequences_bit_exact(matcher):
+    """Runs of equal-length S=32 / S=64 sequences share one attention tile (block-diagonal
+    packing, attention.cuh); mixed with unpackable lengths and padded rows (att < S)."""
+    arch, model = matcher
+    eng = _engine(arch)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
+    rng = np.random.default_rng(29)
+    specs = [(64, 64), (64, 20), (32, 32), (32, 5), (32, 32), (32, 17), (32, 32), (40, 33),
+             (64, 64), (64, 1), (64, 64), (16, 16), (32, 0), (32, 32)]
+    encs = [EncodedInput(rng.integers(4, 1000, S).tolist(), [0] * (S // 2) + [1] * (S - S // 2), att)
+            for S, att in specs]
+    batch = eng.run_batch(encs, plan)
+    for s, enc in enumerate(encs):
+        want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
+        np.testing.assert_array_equal(batch.sequence(s), want, err_msg=f"seq {s} spec {specs[s]}")
+    # same sequences one at a time (single-sequence tiles) give the same bits
+    for s in (1, 3, 12):
+        np.testing.assert_array_equal(eng.run(encs[s], plan).hidden_states, batch.sequence(s))

@@ -5,8 +5,9 @@ import sys
 from collections import defaultdict
 
 
-def main(rep, top=30):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+def main(rep, top=30, kern=None):
+    filt = ["--kernel-name", f"regex:{kern}", "--launch-count", "1"] if kern else []
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + filt,
                          capture_output=True, text=True).stdout
     cur_file, hdr = None, None
     agg = defaultdict(lambda: [0.0, 0.0, ""])
@@ -36,9 +37,10 @@ def main(rep, top=30):
         except (ValueError, TypeError):
             pass
     tot = sum(v[0] for v in agg.values()) or 1
-    for (f, ln), (s, n, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print(f"total warp instructions {sum(v[1] for v in agg.values()):.0f}")
+    for (f, ln), (s, n, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
         print(f"{s / tot * 100:5.1f}% inst={n:10.0f} {f[:14]}:{ln:>4} {src.strip()[:90]}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30, sys.argv[3] if len(sys.argv) > 3 else None)

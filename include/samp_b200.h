@@ -134,6 +134,8 @@ int samp_debug_div_exhaustive(const float* divisors, int n, unsigned long long* 
 int samp_debug_exp_exhaustive(unsigned long long* mismatches);
 /* gelu8_finite (FFN1 epilogue fast path) vs the general numpy-exact GELU, all |x| < 1e12 */
 int samp_debug_gelu_finite_exhaustive(unsigned long long* mismatches);
+/* softmax fast exp (FFMA2, exponent add) vs numpy exp over [-86.5, 0]: mismatches[0] unrefined, [1] refined reciprocal */
+int samp_debug_exp2_fast_exhaustive(unsigned long long* mismatches);
 int samp_debug_unary(int fn, const float* x, float* y, long n);
 
 /* number of kernel launches issued by the last samp_forward (for bench gpu_launches) */

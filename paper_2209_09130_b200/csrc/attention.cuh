@@ -35,6 +35,7 @@
 
 #include <cuda_fp16.h>
 
+#include "gemm.cuh"   // phase-stamp helpers (globaltimer, smid, GEMM_STAMPS)
 #include "numerics.cuh"
 #include "sm100.cuh"
 
@@ -60,6 +61,7 @@ struct AttnParams {
   float* amax;                // FP16 calibration: site amax array (null = off)
   int site_sm, site_ctx;      // L.attn.softmax / L.attn.out_in
   X2 k = x2_consts();         // opaque FFMA2 constants (numerics.cuh)
+  unsigned long long* stamps = nullptr;   // measurement only: 8 %globaltimer stamps per CTA
 };
 
 template <bool F16>
@@ -90,50 +92,15 @@ struct AttnLayout {
 // named barrier among the 256 softmax threads
 __device__ __forceinline__ void att_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-constexpr float ATT_EXP_FAST_MIN = -86.5f;          // x - max >= this  =>  k >= -125 (normal result)
+constexpr float ATT_EXP_FAST_MIN = NP_EXP2_FAST_MIN;   // x - max >= this: np_exp2_fast is exact
 constexpr float ATT_EXP_LO_CUT = -103.97208404541015625f;
 constexpr float ATT_MASK = -10000.0f;
 
-// np_expf_nonpos on a pair whose arguments lie in [ATT_EXP_FAST_MIN, 0]: the clamp and the
-// underflow select are unreachable and p * 2^k (k >= -125, p in [0.7, 1.42]) is normal, so
-// numpy's scalef reduces to an exact exponent add.  Every other operation is the scalar
-// restatement's (numerics.cuh np_expf) on FFMA2 lanes: bit-identical on that domain.
-__device__ __forceinline__ float2 np_exp2_fast(float2 d, const X2& k) {
-  const float2 kk0 = add2(mul2(d, f2(1.442695040888963407359924681001892137f, 1.442695040888963407359924681001892137f), k),
-                          f2(12582912.0f, 12582912.0f), k);
-  const int k0 = __float_as_int(kk0.x) - 0x4B400000, k1 = __float_as_int(kk0.y) - 0x4B400000;
-  const float2 kk = add2(kk0, f2(-12582912.0f, -12582912.0f), k);
-  float2 r = __ffma2_rn(kk, f2(-6.93145752e-1f, -6.93145752e-1f), d);
-  r = __ffma2_rn(kk, f2(-1.42860677e-6f, -1.42860677e-6f), r);
-  r = __ffma2_rn(kk, f2(0.0f, 0.0f), r);
-  float2 num = __ffma2_rn(f2(5.082762527590693718096e-04f, 5.082762527590693718096e-04f), r,
-                          f2(6.757896990527504603057e-03f, 6.757896990527504603057e-03f));
-  num = __ffma2_rn(num, r, f2(5.114512081637298353406e-02f, 5.114512081637298353406e-02f));
-  num = __ffma2_rn(num, r, f2(2.473615434895520810817e-01f, 2.473615434895520810817e-01f));
-  num = __ffma2_rn(num, r, f2(7.257664613233124478488e-01f, 7.257664613233124478488e-01f));
-  num = __ffma2_rn(num, r, f2(9.999999999980870924916e-01f, 9.999999999980870924916e-01f));
-  float2 den = __ffma2_rn(f2(2.159509375685829852307e-02f, 2.159509375685829852307e-02f), r,
-                          f2(-2.742335390411667452936e-01f, -2.742335390411667452936e-01f));
-  den = __ffma2_rn(den, r, f2(1.0f, 1.0f));
-  // make_recip(den) + div_fast(num, .) per lane
-  const float2 r0 = f2(rcp_approx_ftz(den.x), rcp_approx_ftz(den.y));
-  const float2 nden = f2(-den.x, -den.y);
-  const float2 rr = __ffma2_rn(r0, __ffma2_rn(nden, r0, f2(1.0f, 1.0f)), r0);
-  const float2 q = __ffma2_rn(num, rr, f2(k.pzero, k.pzero));
-  const float2 p = __ffma2_rn(rr, __ffma2_rn(nden, q, num), q);
-  return f2(__int_as_float(__float_as_int(p.x) + (k0 << 23)), __int_as_float(__float_as_int(p.y) + (k1 << 23)));
-}
-
-// accumulator -> float: INT8 accumulators satisfy |acc| <= 64*128*128 = 2^20, so
-// F32(acc) = (1.5*2^23 + acc) - 1.5*2^23 exactly (an integer add and a packed subtract)
+// accumulator -> float (INT8: I2FP on the ALU pipe, which has slack next to the FFMA2 chain)
 template <bool F16>
-__device__ __forceinline__ float2 acc_pair(uint32_t a, uint32_t b, const X2& k) {
-  if constexpr (F16) {
-    return f2(__uint_as_float(a), __uint_as_float(b));
-  } else {
-    return add2(f2(__int_as_float(0x4B400000 + int(a)), __int_as_float(0x4B400000 + int(b))),
-                f2(-12582912.0f, -12582912.0f), k);
-  }
+__device__ __forceinline__ float2 acc_pair(uint32_t a, uint32_t b, const X2&) {
+  if constexpr (F16) return f2(__uint_as_float(a), __uint_as_float(b));
+  else return f2(__int2float_rn(int(a)), __int2float_rn(int(b)));
 }
 
 // numpy leaf (n <= 128) over e values in TMEM columns [col, col + n) of this thread's
@@ -192,6 +159,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_load + 4);
 
   const int tile = blockIdx.x, head = blockIdx.y;
+  // phase stamps (tools/gemm_phases.py): smid, start, S in TMEM, pass 1, pass 2, sum, P written, exit
+  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned long long* stamp = p.stamps && cta_id < GEMM_STAMP_CTAS ? p.stamps + size_t(cta_id) * GEMM_STAMPS : nullptr;
+  if (stamp && threadIdx.x == 0) {
+    stamp[0] = smid();
+    stamp[1] = globaltimer();
+  }
   const int seq = p.tile_seq[tile];
   const int q0 = p.tile_q0[tile];
   const int cnt = p.tile_cnt[tile];
@@ -281,6 +255,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     const float m = p.mult_scores;
     mbar_wait(bar_s, 0);
     tc_fence_after();
+    const bool stamper = stamp && threadIdx.x == 32;
+    if (stamper) stamp[2] = globaltimer();
 
     // ---- pass 1: extremes of the accumulators over unmasked [0, att) and masked [att, S)
     // (INT8: int32 order == order of x = RN(F32(acc)*m), m > 0; FP16: f32 order likewise)
@@ -331,6 +307,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     const bool fast_row = !live || ((!has_u || __fsub_rn(xval(umin), mx) >= ATT_EXP_FAST_MIN) &&
                                     (!has_m || __fsub_rn(xm, mx) <= ATT_EXP_LO_CUT));
     const bool fast = __all_sync(0xffffffffu, fast_row);
+    if (stamper) stamp[3] = globaltimer();
     const float2 negmx = f2(-mx, -mx), mm = f2(m, m);
 
     // ---- pass 2: e = exp(x - max) -> TMEM (0 past S)
@@ -362,6 +339,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     tc_fence_before();
     att_bar();                                    // every e of the row is in TMEM
     tc_fence_after();
+    if (stamper) stamp[4] = globaltimer();
 
     // ---- numpy pairwise sum over the row's S values (np.sum = 0 + tree)
     float part = 0.0f;
@@ -376,6 +354,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     xch[h * 128 + r] = part;
     att_bar();
     const float denom = S <= 128 ? __fadd_rn(0.0f, xch[r]) : __fadd_rn(0.0f, __fadd_rn(xch[r], xch[128 + r]));
+    if (stamper) stamp[5] = globaltimer();
     // denom in [1, S] and e in [0, 1]: the hoisted-reciprocal quotient is exact (numerics.cuh)
     const Recip rden = make_recip(denom), rsm = make_recip(F16 ? 1.0f : p.s_softmax);
 
@@ -440,6 +419,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
       mbar_arrive(bar_p);
     }
 
+    if (stamper) stamp[6] = globaltimer();
     // context rows: h writes output columns [32h, 32h+32)
     mbar_wait(bar_pf, (nchunks - 1) & 1);
     tc_fence_after();
@@ -490,6 +470,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     tc_fence_after();
     tmem_dealloc(tmem, p.tmem_cols);
   }
+  if (stamp && threadIdx.x == 0) stamp[7] = globaltimer();
 }
 
 }  // namespace samp

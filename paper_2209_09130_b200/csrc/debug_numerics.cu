@@ -85,6 +85,23 @@ __global__ void exp_exhaustive_kernel(unsigned long long* bad) {
   atomicAdd(bad, local);
 }
 
+// np_exp2_fast (both reciprocal variants) against np_expf with the IEEE divide for every
+// float in [NP_EXP2_FAST_MIN, 0] (both zeros included); bad[0] = unrefined, bad[1] = refined
+__global__ void exp2_fast_exhaustive_kernel(unsigned long long* bad, const X2 k) {
+  const uint32_t hi = __float_as_uint(NP_EXP2_FAST_MIN);
+  unsigned long long l0 = 0, l1 = 0;
+  for (uint64_t u = 0x80000000ull + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u <= hi + 1ull;
+       u += uint64_t(gridDim.x) * blockDim.x) {
+    const float x = u == hi + 1ull ? 0.0f : __uint_as_float(uint32_t(u));   // the extra slot = +0
+    const float want = np_expf_ieee(x);
+    const float2 a = np_exp2_fast<false>(f2(x, x), k), b = np_exp2_fast<true>(f2(x, x), k);
+    l0 += (__float_as_uint(a.x) != __float_as_uint(want)) + (__float_as_uint(a.y) != __float_as_uint(want));
+    l1 += (__float_as_uint(b.x) != __float_as_uint(want)) + (__float_as_uint(b.y) != __float_as_uint(want));
+  }
+  atomicAdd(bad, l0);
+  atomicAdd(bad + 1, l1);
+}
+
 // gelu8_finite (and its FFMA2 form) against gelu_ref over every float with |x| < 1e12
 // (the host-proven domain)
 __global__ void gelu_finite_exhaustive_kernel(unsigned long long* bad, const X2 k) {
@@ -168,6 +185,19 @@ extern "C" int samp_debug_div_exhaustive(const float* divisors, int n, unsigned 
 extern "C" int samp_debug_exp_exhaustive(unsigned long long* mismatches) {
   return guarded([&] {
     *mismatches = run_count([](unsigned long long* d) { exp_exhaustive_kernel<<<148 * 8, 256>>>(d); });
+  });
+}
+
+extern "C" int samp_debug_exp2_fast_exhaustive(unsigned long long* mismatches /* [2] */) {
+  return guarded([&] {
+    unsigned long long* d;
+    SAMP_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+    SAMP_CUDA(cudaMemset(d, 0, 2 * sizeof(unsigned long long)));
+    exp2_fast_exhaustive_kernel<<<148 * 8, 256>>>(d, x2_consts());
+    SAMP_CUDA(cudaGetLastError());
+    SAMP_CUDA(cudaDeviceSynchronize());
+    SAMP_CUDA(cudaMemcpy(mismatches, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    cudaFree(d);
   });
 }
 

@@ -357,7 +357,7 @@ static void run_kernel(samp_engine* e, const char* what, F&& fn) {
     SAMP_CUDA(cudaEventRecord(a, e->stream_in_use));
   }
   const bool stamped = e->profiling && e->stamps && int(e->stamp_launches.size()) < e->stamp_cap &&
-                       std::strstr(what, "attention") == nullptr && std::strcmp(what, "embed") != 0 &&
+                       std::strcmp(what, "embed") != 0 &&
                        std::strcmp(what, "head") != 0;
   if (stamped) {
     g_gemm_stamps = e->stamps + size_t(e->stamp_launches.size()) * STAMP_CTAS * GEMM_STAMPS;
@@ -378,8 +378,9 @@ static void run_kernel(samp_engine* e, const char* what, F&& fn) {
 
 static void launch_attention(samp_engine* e, bool f16, const AttnParams& p) {
   const Geometry& g = e->geo;
-  check_launch(e, f16 ? launch_attention_f16(e->act.att_qkv_f16, p, g.ntiles, e->d.num_heads, g.max_nkp, e->stream_in_use)
-                      : launch_attention_i8(e->act.att_qkv_i8, p, g.ntiles, e->d.num_heads, g.max_nkp, e->stream_in_use),
+  auto stamped = [&]() { AttnParams q = p; q.stamps = g_gemm_stamps; return q; };
+  check_launch(e, f16 ? launch_attention_f16(e->act.att_qkv_f16, stamped(), g.ntiles, e->d.num_heads, g.max_nkp, e->stream_in_use)
+                      : launch_attention_i8(e->act.att_qkv_i8, stamped(), g.ntiles, e->d.num_heads, g.max_nkp, e->stream_in_use),
                f16 ? "attention_f16" : "attention_i8");
 }
 

@@ -93,6 +93,18 @@ def test_exp_fast_division_exhaustive():
     assert bad.value == 0
 
 
+def test_exp2_fast_exhaustive():
+    """Softmax fast exp (FFMA2 pairs, exact exponent add, unrefined reciprocal) equals numpy's
+    float32 exp (IEEE divide restatement) for every float in [-86.5, 0]."""
+    import ctypes
+    lib = _lib.load()
+    bad = (ctypes.c_ulonglong * 2)()
+    _lib.check(lib.samp_debug_exp2_fast_exhaustive(bad))
+    print(f"mismatches: unrefined {bad[0]}, refined {bad[1]}")
+    assert bad[1] == 0
+    assert bad[0] == 0
+
+
 def test_gelu_finite_fast_path_exhaustive():
     import ctypes
     lib = _lib.load()

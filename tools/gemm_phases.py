@@ -69,13 +69,14 @@ def main():
         st = buf[i].astype(np.int64)
         st = st[st[:, 1] != 0]
         t0 = st[:, 1].min()
-        span = (st[:, 6].max() - t0) / 1e3
-        ph = np.stack([st[:, 2] - st[:, 1], st[:, 3] - st[:, 2], st[:, 4] - st[:, 3],
-                       st[:, 5] - st[:, 4], st[:, 6] - st[:, 5]], 1) / 1e3
+        att = name.startswith("attention")
+        end = 7 if att else 6     # attention: stamp 7 = exit (1 start, 2 S ready, 3-6 softmax passes)
+        span = (st[:, end].max() - t0) / 1e3
+        ph = np.stack([st[:, j + 1] - st[:, j] for j in range(1, end)], 1) / 1e3
         # residency: max CTAs of this launch alive on one SM at the same time
         per_sm = defaultdict(list)
         for row in st:
-            per_sm[int(row[0])].append((row[1], row[6]))
+            per_sm[int(row[0])].append((row[1], row[end]))
         conc = 0
         for iv in per_sm.values():
             ev = sorted([(a, 1) for a, _ in iv] + [(b, -1) for _, b in iv], key=lambda x: (x[0], x[1]))
@@ -88,6 +89,7 @@ def main():
         agg[name].append((span, len(st), len(per_sm), conc, last_start, ph.mean(0), ph.max(0)))
     print(f"{'gemm':12s} {'span_us':>8s} {'ctas':>5s} {'sms':>4s} {'conc':>4s} {'lastst':>7s} | "
           f"{'fill':>6s} {'loads':>6s} {'drain':>6s} {'epi':>6s} {'tear':>6s}  (mean per CTA, us; max in [])")
+    print(f"{'':52s}attention phases: load+MMA1, pass1, pass2, sum, pass3, MMA2+out")
     for name, rows in agg.items():
         span = np.mean([r[0] for r in rows])
         ph = np.mean([r[5] for r in rows], 0)

@@ -136,6 +136,11 @@ int samp_debug_exp_exhaustive(unsigned long long* mismatches);
 int samp_debug_gelu_finite_exhaustive(unsigned long long* mismatches);
 /* softmax fast exp (FFMA2, exponent add) vs numpy exp over [-86.5, 0]: mismatches[0] unrefined, [1] refined reciprocal */
 int samp_debug_exp2_fast_exhaustive(unsigned long long* mismatches);
+/* FFN1 fast GELU epilogue admission check for one ffn.mid scale (every float |x| < 1e12):
+ * counts[0] = unflagged elements whose fast code differs from the exact one (0 = admitted),
+ * counts[1] = flagged elements (recomputed exactly by the kernel).  Replaces nothing in the
+ * reference: it proves GELU_FAST equal to quantize(gelu(x), s) (encoder.py:406-410). */
+int samp_debug_gelu_fast_check(float s, unsigned long long* counts);
 int samp_debug_unary(int fn, const float* x, float* y, long n);
 
 /* number of kernel launches issued by the last samp_forward (for bench gpu_launches) */

@@ -74,6 +74,7 @@ SIGNATURES = [
     ("samp_debug_exp_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_gelu_finite_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_exp2_fast_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
+    ("samp_debug_gelu_fast_check", ctypes.c_int, [ctypes.c_float, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_unary", ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long]),
     ("samp_last_launch_count", ctypes.c_int, [ctypes.c_void_p]),
     ("samp_set_profiling", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

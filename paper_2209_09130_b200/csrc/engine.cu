@@ -162,6 +162,8 @@ struct samp_engine {
   };
   bool graphs_enabled = true;
   std::map<std::string, GraphEntry> graphs;   // (plan, geometry, head) -> captured forward
+  // ffn.mid scale (bits) -> GELU_FAST admitted (exhaustive check, gelu_fast_check)
+  std::map<uint32_t, bool> gelu_fast_ok;
   std::set<std::string> seen;
   struct Pending { std::string name; cudaEvent_t a, b; };
   std::vector<Pending> pending;
@@ -350,6 +352,10 @@ constexpr int STAMP_CTAS = GEMM_STAMP_CTAS;   // CTAs recorded per stamped GEMM 
 // events on the engine stream (the stream every kernel is launched on)
 template <class F>
 static void run_kernel(samp_engine* e, const char* what, F&& fn) {
+  // measurement only: SAMP_SKIP=name[,name] drops those launches (results are garbage; the
+  // step-time difference is the kernels' share of the pipelined critical path)
+  static const std::string skip = std::getenv("SAMP_SKIP") ? "," + std::string(std::getenv("SAMP_SKIP")) + "," : "";
+  if (!skip.empty() && skip.find("," + std::string(what) + ",") != std::string::npos) return;
   cudaEvent_t a = nullptr, b = nullptr;
   if (e->profiling) {
     a = take_event(e);
@@ -388,6 +394,29 @@ static int tmem_cols_for_keys(int nkp) {
   int c = 64;
   while (c < nkp) c *= 2;
   return c;
+}
+
+static uint32_t bits_of(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
+static float gelu_inv_s(float s) { return float(1.0 / double(s)); }
+
+// Admit GELU_FAST for every INT8-FFN layer's ffn.mid scale of this plan (exhaustive device
+// check per distinct scale, cached for the engine's lifetime).  SAMP_NO_GELU_FAST=1 keeps
+// the exact epilogue everywhere (A/B measurements).
+static void gelu_fast_prepare(samp_engine* e, const uint8_t* prec) {
+  static const bool off = std::getenv("SAMP_NO_GELU_FAST") != nullptr;
+  if (off) return;
+  for (int i = 0; i < e->d.num_layers; ++i) {
+    if (prec[i] != SAMP_LAYER_FULL_INT8 && prec[i] != SAMP_LAYER_FFN_INT8) continue;
+    const float s = f32(sc(e, lsite(i, "ffn", "mid")));
+    if (e->gelu_fast_ok.count(bits_of(s))) continue;
+    unsigned long long counts[2] = {1, 0};
+    SAMP_CUDA(gelu_fast_check(s, gelu_inv_s(s), counts, e->stream));
+    e->gelu_fast_ok[bits_of(s)] = counts[0] == 0;
+  }
 }
 
 // one encoder layer; `in_q` = index of xq holding this layer's input codes (INT8 inputs)
@@ -520,8 +549,14 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     // |x| <= K * 128^2 * |mult| + max|b1| far below where C*(x + K x^3) overflows: the
     // GELU's inf/nan path is unreachable (gelu8_finite)
     const bool finite = double(H) * 16384.0 * std::fabs(double(gp.mult)) + w.b1_absmax < 1e12;
+    // codes from the MUFU GELU with exact fallback on flagged elements, when this scale
+    // passed the exhaustive admission check (gelu_fast_prepare, before any capture)
+    auto ok = e->gelu_fast_ok.find(bits_of(gp.s_out));
+    const bool fast = finite && ok != e->gelu_fast_ok.end() && ok->second;
+    gp.inv_s = gelu_inv_s(gp.s_out);
     const int k1 = ffn1_bn_index(T, I, e->sms);
-    check_launch(e, gemm_gelu_i8(FFN1_BN[k1], finite, a.a_ffn_in, w.m_w1_i8[k1], T, I, H, gp, st), "ffn1_i8");
+    check_launch(e, gemm_gelu_i8(FFN1_BN[k1], fast ? GELU_FAST : finite ? GELU_FINITE : GELU_GENERAL, a.a_ffn_in,
+                                 w.m_w1_i8[k1], T, I, H, gp, st), "ffn1_i8");
     record(e, "mid_q", i, a.mid_i8, size_t(T) * I);
     lp.res_i8 = a.ffn_in_i8;
     lp.res_scale = f32(s_fin);
@@ -787,6 +822,10 @@ extern "C" int samp_clear_calibration(samp_engine* e) {
   });
 }
 
+extern "C" int samp_debug_gelu_fast_check(float s, unsigned long long* counts) {
+  return guarded([&] { SAMP_CUDA(gelu_fast_check(s, gelu_inv_s(s), counts, nullptr)); });
+}
+
 extern "C" int samp_set_graphs(samp_engine* e, int on) {
   return guarded([&] {
     clear_graphs(e);
@@ -980,6 +1019,7 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       SAMP_CUDA(cudaMemcpyAsync(a.ids, ids, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
       SAMP_CUDA(cudaMemcpyAsync(a.segs, segs, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
     }
+    gelu_fast_prepare(e, prec);
     // ---------------- device work: replay a captured CUDA graph for this (plan, batch
     // geometry, head) when one exists; capture on the second sighting of a key (the first
     // run also configures every kernel's smem attributes outside of capture)

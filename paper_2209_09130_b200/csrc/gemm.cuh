@@ -330,17 +330,21 @@ struct EpiQKV {
 };
 
 // FFN1: F32(acc)*mult + b1 -> GELU (numpy/SVML-exact) -> quantize(ffn.mid)
-// (reference encoder.py:406-410).  FINITE: the host proved the GELU argument finite for
-// this launch (gelu8_finite); otherwise the general gelu8 (inf/nan-capable) runs.
+// (reference encoder.py:406-410).  MODE 0: general gelu8 (inf/nan-capable); MODE 1
+// (GELU_FINITE): the host proved the GELU argument finite for this launch (gelu8_finite);
+// MODE 2 (GELU_FAST): additionally the scale passed the exhaustive fast-path check, so
+// codes come from gelu_q_fast2 and only flagged elements take the exact path.
+enum { GELU_GENERAL = 0, GELU_FINITE = 1, GELU_FAST = 2 };
 struct GeluQuantParams {
   int8_t* out;
   int ldo;
   const float* bias;
   float mult;
   float s_out;
+  float inv_s = 0.0f;   // ~1/s_out (GELU_FAST)
   X2 k = x2_consts();   // opaque FFMA2 constants (packed path)
 };
-template <bool FINITE>
+template <int MODE>
 struct EpiGeluQuantT {
   using Params = GeluQuantParams;
   template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
@@ -349,6 +353,19 @@ struct EpiGeluQuantT {
   __device__ static void prefetch(const Params& p, uint8_t* smem, int, int n0, int, int tid, int nt) {
     load_tanh_table(reinterpret_cast<TanhTable*>(smem), tid, nt);
     stage_floats(reinterpret_cast<float*>(smem + sizeof(TanhTable)), p.bias + n0, BN, tid, nt);
+  }
+  // exact codes of 8 finite GELU arguments (packed FFMA2 arithmetic, see numerics.cuh)
+  __device__ static void exact8(const float (&x)[8], const TanhTable* tt, const Recip& rq, const X2& k,
+                                uint32_t& w0, uint32_t& w1) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = x[u];
+    gelu8_finite_x2(v, tt, k);
+    float2 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = quant_pre2(f2(v[2 * u], v[2 * u + 1]), rq, k);
+    w0 = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
+    w1 = trunc_pack4_s8(q[2].x, q[2].y, q[3].x, q[3].y);
   }
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
@@ -359,13 +376,15 @@ struct EpiGeluQuantT {
 #ifndef SAMP_GELU_CHUNK
 #define SAMP_GELU_CHUNK 16
 #endif
-    constexpr int CH = (BN / (NE / 4)) % SAMP_GELU_CHUNK == 0 ? SAMP_GELU_CHUNK : 16;
+    constexpr int COLS = BN / (NE / 4);
+    constexpr int CH = COLS % SAMP_GELU_CHUNK == 0 ? SAMP_GELU_CHUNK : COLS % 16 == 0 ? 16 : 8;
 #pragma unroll 1
     for (int col = 0; col < c.ncols; col += CH) {
       const int gcol = c.n0 + c.c0 + col;
       uint32_t r[CH];
       if constexpr (CH == 32) tmem_ld32(c.taddr + col, r);
-      else tmem_ld16(c.taddr + col, r);
+      else if constexpr (CH == 16) tmem_ld16(c.taddr + col, r);
+      else tmem_ld8(c.taddr + col, r);
       float b[CH];
 #pragma unroll
       for (int j = 0; j < CH / 4; ++j) {
@@ -377,7 +396,7 @@ struct EpiGeluQuantT {
 #pragma unroll
       for (int g = 0; g < CH; g += 8) {
         float v[8];
-        if constexpr (FINITE) {   // packed (FFMA2) arithmetic, see numerics.cuh
+        if constexpr (MODE != GELU_GENERAL) {   // packed (FFMA2) arithmetic, see numerics.cuh
           const X2 k = p.k;
 #pragma unroll
           for (int u = 0; u < 8; u += 2) {
@@ -387,12 +406,20 @@ struct EpiGeluQuantT {
             v[u] = d.x;
             v[u + 1] = d.y;
           }
-          gelu8_finite_x2(v, tt, k);
-          float2 q[4];
+          if constexpr (MODE == GELU_FAST) {
+            bool near = false;
+            float2 t[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) q[u] = quant_pre2(f2(v[2 * u], v[2 * u + 1]), rq, k);
-          w[g / 4] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
-          w[g / 4 + 1] = trunc_pack4_s8(q[2].x, q[2].y, q[3].x, q[3].y);
+            for (int u = 0; u < 4; ++u) t[u] = gelu_q_fast2(f2(v[2 * u], v[2 * u + 1]), p.inv_s, k, near);
+            if (near) {
+              exact8(v, tt, rq, k, w[g / 4], w[g / 4 + 1]);
+            } else {
+              w[g / 4] = trunc_pack4_s8(t[0].x, t[0].y, t[1].x, t[1].y);
+              w[g / 4 + 1] = trunc_pack4_s8(t[2].x, t[2].y, t[3].x, t[3].y);
+            }
+          } else {
+            exact8(v, tt, rq, k, w[g / 4], w[g / 4 + 1]);
+          }
         } else {
 #pragma unroll
           for (int u = 0; u < 8; ++u) v[u] = __fadd_rn(__fmul_rn(__int2float_rn(int(r[g + u])), p.mult), b[g + u]);
@@ -404,16 +431,21 @@ struct EpiGeluQuantT {
         }
       }
       if (c.row < c.M) {
-        uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
+        if constexpr (CH == 8) {
+          *reinterpret_cast<uint2*>(p.out + size_t(c.row) * p.ldo + gcol) = make_uint2(w[0], w[1]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
 #pragma unroll
-        for (int q = 0; q < CH / 16; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          for (int q = 0; q < CH / 16; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        }
       }
     }
   }
 };
 
-using EpiGeluQuant = EpiGeluQuantT<false>;
-using EpiGeluQuantFinite = EpiGeluQuantT<true>;
+using EpiGeluQuant = EpiGeluQuantT<GELU_GENERAL>;
+using EpiGeluQuantFinite = EpiGeluQuantT<GELU_FINITE>;
+using EpiGeluQuantFast = EpiGeluQuantT<GELU_FAST>;
 
 // FP16-path bias (+ optional GELU) epilogue: acc(F32) + bias [-> gelu] -> f16 storage.
 // (reference mha_fp encoder.py:291-292 qkv = gemm + qkv_b; ffn_fp :325-326 gelu(mid))

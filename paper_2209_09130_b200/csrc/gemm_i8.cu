@@ -9,6 +9,9 @@ namespace samp {
 #ifndef SAMP_PERSIST_NE
 #define SAMP_PERSIST_NE 8
 #endif
+#ifndef SAMP_FFN1_NE96
+#define SAMP_FFN1_NE96 8
+#endif
 
 // persistent (gemm_persistent.cuh) unless SAMP_NO_PERSISTENT is set (A/B measurements)
 inline bool persistent_enabled() {
@@ -24,7 +27,7 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
     switch (bn) {
       case 256: return launch_gemm_persistent<KIND_I8, 256, 4, NEP, Epi>(a, b, M, N, kb, p, st);
       case 128: return launch_gemm_persistent<KIND_I8, 128, SAMP_PERSIST_STAGES128, NEP, Epi>(a, b, M, N, kb, p, st);
-      case 96: return launch_gemm_persistent<KIND_I8, 96, 6, 8, Epi>(a, b, M, N, kb, p, st);
+      case 96: return launch_gemm_persistent<KIND_I8, 96, 6, SAMP_FFN1_NE96, Epi>(a, b, M, N, kb, p, st);
       case 64: return launch_gemm_persistent<KIND_I8, 64, 6, 8, Epi>(a, b, M, N, kb, p, st);
     }
     return cudaErrorInvalidValue;
@@ -44,10 +47,56 @@ cudaError_t gemm_qkv_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int 
   return by_bn<EpiQKV>(bn, false, a, b, M, N, kb, p, st);
 }
 
-cudaError_t gemm_gelu_i8(int bn, bool finite, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+cudaError_t gemm_gelu_i8(int bn, int mode, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                          const EpiGeluQuant::Params& p, cudaStream_t st) {
-  if (finite) return by_bn<EpiGeluQuantFinite>(bn, true, a, b, M, N, kb, p, st);
+  if (mode == GELU_FAST) return by_bn<EpiGeluQuantFast>(bn, true, a, b, M, N, kb, p, st);
+  if (mode == GELU_FINITE) return by_bn<EpiGeluQuantFinite>(bn, true, a, b, M, N, kb, p, st);
   return by_bn<EpiGeluQuant>(bn, true, a, b, M, N, kb, p, st);
+}
+
+// Exhaustive admission check of the GELU_FAST epilogue for one ffn.mid scale: every float x
+// with |x| < 1e12 (the FINITE domain), each element's own near-flag; counts[0] = elements
+// whose unflagged fast code differs from the exact code (must be 0), counts[1] = flagged.
+__global__ void gelu_fast_exhaustive_kernel(float s, float inv_s, X2 k, unsigned long long* counts) {
+  __shared__ TanhTable tt;
+  load_tanh_table(&tt, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const Recip rq = make_recip(s);
+  unsigned long long bad = 0, flagged = 0;
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < (1ull << 29);
+       g += uint64_t(gridDim.x) * blockDim.x) {
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x[u] = __uint_as_float(uint32_t(g * 8 + u));
+      if (!(fabsf(x[u]) < 1e12f)) x[u] = 0.0f;
+    }
+    uint32_t e0, e1;
+    EpiGeluQuantFast::exact8(x, &tt, rq, k, e0, e1);
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      bool near = false;
+      const float2 t = gelu_q_fast2(f2(x[u], x[u + 1]), inv_s, k, near);
+      const uint32_t fq = trunc_pack4_s8(t.x, t.y, 0.0f, 0.0f);
+      const uint32_t ex = (u < 4 ? e0 : e1) >> (8 * (u & 3));
+      flagged += near;
+      bad += !near && ((fq ^ ex) & 0xffffu) != 0u;
+    }
+  }
+  atomicAdd(counts, bad);
+  atomicAdd(counts + 1, flagged);
+}
+
+cudaError_t gelu_fast_check(float s, float inv_s, unsigned long long* host_counts, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  cudaError_t err = cudaMallocAsync(&d, 2 * sizeof(unsigned long long), st);
+  if (err != cudaSuccess) return err;
+  cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), st);
+  gelu_fast_exhaustive_kernel<<<148 * 8, 256, 0, st>>>(s, inv_s, x2_consts(), d);
+  cudaMemcpyAsync(host_counts, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  err = cudaStreamSynchronize(st);
+  return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 }  // namespace samp

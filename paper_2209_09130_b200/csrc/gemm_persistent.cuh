@@ -56,7 +56,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(2 * BN <= 512 && BN % 16 == 0, "two accumulators must fit TMEM");
   static_assert(NE == 8 || NE == 16, "epilogue warps");
-  static_assert((BN / PARTS) % 16 == 0, "epilogue column chunks");
+  static_assert((BN / PARTS) % 8 == 0, "epilogue column chunks");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);

@@ -18,7 +18,9 @@ struct Tiles {
 cudaError_t gemm_qkv_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                         const EpiQKV::Params& p, cudaStream_t st);
 // finite: |acc*mult + bias| is bounded well below the GELU overflow (host check)
-cudaError_t gemm_gelu_i8(int bn, bool finite, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+// exhaustive admission check of the FFN1 fast GELU epilogue for one scale (gemm_i8.cu)
+cudaError_t gelu_fast_check(float s, float inv_s, unsigned long long* host_counts /*[2]*/, cudaStream_t st);
+cudaError_t gemm_gelu_i8(int bn, int mode, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                          const EpiGeluQuant::Params& p, cudaStream_t st);
 // gemm_ln.cu
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,

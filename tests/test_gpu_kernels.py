@@ -105,6 +105,26 @@ def test_exp2_fast_exhaustive():
     assert bad[0] == 0
 
 
+def test_gelu_fast_admission_all_bench_scales():
+    """FFN1 fast GELU epilogue (MUFU gelu + margin flag, exact fallback): for every ffn.mid
+    scale of the bench calibration plus extremes, no unflagged element over all floats
+    |x| < 1e12 differs from quantize(gelu(x), s).  The engine runs this same check per scale
+    before it may launch GELU_FAST (gelu_fast_prepare)."""
+    import ctypes
+    import json
+    import os
+    lib = _lib.load()
+    path = os.path.join(os.path.dirname(__file__), "golden", "bench_calibration_bert-base.json")
+    sites = json.load(open(path))["sites"]
+    scales = [float(np.float32(max(v["amax"], 127e-8) / 127.0)) for k, v in sites.items() if k.endswith("ffn.mid")]
+    scales += [float(np.float32(x)) for x in (1e-8, 1e-4, 0.01, 0.5, 3.0, 100.0)]
+    counts = (ctypes.c_ulonglong * 2)()
+    for s in scales:
+        _lib.check(lib.samp_debug_gelu_fast_check(ctypes.c_float(s), counts))
+        print(f"s={s:.4g}: mismatches {counts[0]}, flagged {counts[1]} ({counts[1] / 2**32:.2e})")
+        assert counts[0] == 0
+
+
 def test_gelu_finite_fast_path_exhaustive():
     import ctypes
     lib = _lib.load()

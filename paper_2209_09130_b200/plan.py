@@ -11,6 +11,8 @@ are flagged as an extension wherever reported.
 
 from __future__ import annotations
 
+import functools
+
 from dataclasses import dataclass
 
 from .errors import ConfigurationError
@@ -94,18 +96,29 @@ class PrecisionPlan:
         return EMBED_OUT_SITE if i == 0 else attn_in_site(i)
 
     def required_sites(self) -> set:
-        need = set()
-        for i, p in enumerate(self.layer_precisions):
-            if p in (LAYER_FULL_INT8, LAYER_MHA_INT8):
-                need.add(self.input_site(i))
-                need.update(attn_site(i, n) for n in ATTN_NAMES)
-                need.add(ffn_site(i, "in"))
-                if p == LAYER_FULL_INT8:
-                    need.add(ffn_site(i, "mid"))
-            elif p == LAYER_FFN_INT8:
-                need.update((ffn_site(i, "in"), ffn_site(i, "mid")))
-        return need
+        return set(_required_sites(self.layer_precisions))
 
     def codes(self) -> bytes:
         """Per-layer precision codes for the C-ABI."""
-        return bytes(LAYER_CODE[p] for p in self.layer_precisions)
+        return _codes(self.layer_precisions)
+
+
+@functools.lru_cache(maxsize=256)
+def _codes(layer_precisions: tuple) -> bytes:
+    return bytes(LAYER_CODE[p] for p in layer_precisions)
+
+
+@functools.lru_cache(maxsize=256)
+def _required_sites(layer_precisions: tuple) -> frozenset:
+    """Sites a plan reads (reference encoder.py:126-136); cached per plan (hot per forward)."""
+    need = set()
+    for i, p in enumerate(layer_precisions):
+        if p in (LAYER_FULL_INT8, LAYER_MHA_INT8):
+            need.add(EMBED_OUT_SITE if i == 0 else attn_in_site(i))
+            need.update(attn_site(i, n) for n in ATTN_NAMES)
+            need.add(ffn_site(i, "in"))
+            if p == LAYER_FULL_INT8:
+                need.add(ffn_site(i, "mid"))
+        elif p == LAYER_FFN_INT8:
+            need.update((ffn_site(i, "in"), ffn_site(i, "mid")))
+    return frozenset(need)

@@ -75,10 +75,12 @@ static int pick_bn(int n) {
   return 0;
 }
 
-// FFN1 runs persistent (one CTA per SM walking tiles); its makespan is the per-CTA tile
-// count times the tile width, so the width is picked per launch from these
+// FFN1 runs persistent (walking tiles); its makespan is the per-CTA tile count times the
+// tile width, so the width is picked per launch from these (costed per SM: with two INT8
+// CTAs per SM the SM-level balance is what matters; measured 96-wide at 4096 tokens)
 constexpr int FFN1_BN[3] = {64, 96, 128};
-static int ffn1_bn_index(int T, int I, int sms, bool allow96 = true) {
+static int ffn1_bn_index(int T, int I, int slots, bool allow96 = true) {
+  const int sms = slots;
   const int mt = (T + GEMM_BM - 1) / GEMM_BM;
   int best = -1;
   long best_cost = 0;

@@ -3,15 +3,10 @@
 
 namespace samp {
 
-#ifndef SAMP_PERSIST_STAGES128
-#define SAMP_PERSIST_STAGES128 5
-#endif
 #ifndef SAMP_PERSIST_NE
 #define SAMP_PERSIST_NE 8
 #endif
-#ifndef SAMP_FFN1_NE96
-#define SAMP_FFN1_NE96 8
-#endif
+
 
 // persistent (gemm_persistent.cuh) unless SAMP_NO_PERSISTENT is set (A/B measurements)
 inline bool persistent_enabled() {
@@ -24,11 +19,12 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
                          const typename Epi::Params& p, cudaStream_t st) {
   constexpr int NEP = SAMP_PERSIST_NE;
   if (persistent && persistent_enabled()) {
+    // two persistent CTAs per SM where the ring fits twice (<= ~100 KB each)
     switch (bn) {
       case 256: return launch_gemm_persistent<KIND_I8, 256, 4, NEP, Epi>(a, b, M, N, kb, p, st);
-      case 128: return launch_gemm_persistent<KIND_I8, 128, SAMP_PERSIST_STAGES128, NEP, Epi>(a, b, M, N, kb, p, st);
-      case 96: return launch_gemm_persistent<KIND_I8, 96, 6, SAMP_FFN1_NE96, Epi>(a, b, M, N, kb, p, st);
-      case 64: return launch_gemm_persistent<KIND_I8, 64, 6, 8, Epi>(a, b, M, N, kb, p, st);
+      case 128: return launch_gemm_persistent<KIND_I8, 128, 3, NEP, Epi, 2>(a, b, M, N, kb, p, st);
+      case 96: return launch_gemm_persistent<KIND_I8, 96, 3, 8, Epi, 2>(a, b, M, N, kb, p, st);
+      case 64: return launch_gemm_persistent<KIND_I8, 64, 4, 8, Epi, 2>(a, b, M, N, kb, p, st);
     }
     return cudaErrorInvalidValue;
   }

@@ -132,15 +132,55 @@ __device__ __forceinline__ float pairwise_warp(V& v) {
   return ct_combine<H, 0>(leafval);
 }
 
+// Uniform-leaf fast path: when numpy's tree over H ends in NL equal leaves of LEN (H = 768:
+// 8 x 96, 1024: 8 x 128, 512: 4 x 128, 384: 4 x 96), the four 8-lane groups reduce four
+// leaves at once (round rd: group q owns leaf 4*rd + q) instead of one group per leaf with
+// the other 24 lanes masked off.  The row lives in smem with 8 pad floats after every leaf
+// (emb_pad) so the four groups' reads fall in distinct banks.
+template <int H>
+struct EmbLeaves {
+  static constexpr int NL = ct_leaves(H);
+  static constexpr int LEN = H / NL;
+  static constexpr bool uniform = NL >= 2 && NL <= 8 && H % NL == 0 && LEN % 8 == 0 && pw_splits_evenly(H, NL);
+  static constexpr int ROW = uniform ? H + 8 * NL : H;   // smem floats per token row
+};
+template <int H>
+__device__ __forceinline__ int emb_pad(int i) {
+  if constexpr (EmbLeaves<H>::uniform) return i + (i / EmbLeaves<H>::LEN) * 8;
+  else return i;
+}
+
+template <int H, class V>
+__device__ __forceinline__ float pairwise_warp_uniform(V& v) {
+  using EL = EmbLeaves<H>;
+  constexpr int NL = EL::NL, LEN = EL::LEN, ROUNDS = (NL + 3) / 4;
+  const int lane = threadIdx.x & 31, grp = lane >> 3, g = lane & 7;
+  float mine[ROUNDS];
+#pragma unroll
+  for (int rd = 0; rd < ROUNDS; ++rd) {
+    const int li = rd * 4 + grp;
+    const int lo = (li < NL ? li : 0) * LEN;
+    float acc = v(lo + g);
+#pragma unroll
+    for (int i = 8; i < LEN; i += 8) acc = __fadd_rn(acc, v(lo + i + g));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    mine[rd] = acc;
+  }
+  auto leafval = [&](int li) { return __shfl_sync(0xffffffffu, mine[li >> 2], (li & 3) * 8); };
+  return ct_combine<H, 0>(leafval);
+}
+
 template <int H>
 static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedParams p) {
-  extern __shared__ float xs[];              // [8 warps][H]
+  extern __shared__ float xs[];              // [8 warps][EmbLeaves<H>::ROW]
   pdl_trigger();
   pdl_wait();                                 // xq / hidden buffers are still read by the previous forward
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * (EMB_THREADS / 32) + warp;
   if (t >= p.T) return;                       // warp-uniform
-  float* row = xs + warp * H;
+  float* row = xs + warp * EmbLeaves<H>::ROW;
   {
     const float* w = p.word + size_t(p.ids[t]) * H;
     const float* ps = p.position + size_t(p.pos[t]) * H;
@@ -150,26 +190,39 @@ static __global__ void __launch_bounds__(EMB_THREADS) embed_kernel(const EmbedPa
       const float4 a = __ldg(reinterpret_cast<const float4*>(w + c));
       const float4 b = __ldg(reinterpret_cast<const float4*>(ps + c));
       const float4 d = __ldg(reinterpret_cast<const float4*>(ty + c));
-      *reinterpret_cast<float4*>(row + c) = make_float4(
+      *reinterpret_cast<float4*>(row + emb_pad<H>(c)) = make_float4(
           __fadd_rn(__fadd_rn(a.x, b.x), d.x), __fadd_rn(__fadd_rn(a.y, b.y), d.y),
           __fadd_rn(__fadd_rn(a.z, b.z), d.z), __fadd_rn(__fadd_rn(a.w, b.w), d.w));
     }
   }
   __syncwarp();
-  auto vx = [&](int i) { return row[i]; };
   const float hf = float(H);
-  const float mean = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp<H>(vx)), hf);
-  auto vc = [&](int i) {
-    const float d = __fsub_rn(row[i], mean);
-    return __fmul_rn(d, d);
-  };
-  const float var = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp<H>(vc)), hf);
+  float mean, var;
+  if constexpr (EmbLeaves<H>::uniform) {
+    // leaf-local index i of leaf li sits at li*(LEN+8) + i: v(lo + i) with lo = li*LEN
+    auto at = [&](int i) { return row[emb_pad<H>(i)]; };
+    auto vx = [&](int i) { return at(i); };
+    mean = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp_uniform<H>(vx)), hf);
+    auto vc = [&](int i) {
+      const float d = __fsub_rn(at(i), mean);
+      return __fmul_rn(d, d);
+    };
+    var = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp_uniform<H>(vc)), hf);
+  } else {
+    auto vx = [&](int i) { return row[i]; };
+    mean = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp<H>(vx)), hf);
+    auto vc = [&](int i) {
+      const float d = __fsub_rn(row[i], mean);
+      return __fmul_rn(d, d);
+    };
+    var = __fdiv_rn(__fadd_rn(0.0f, pairwise_warp<H>(vc)), hf);
+  }
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
   const Recip rq = make_recip(p.out_i8 ? p.s_out : 1.0f);
   const size_t base = size_t(t) * H;
   float amx = 0.0f;
   for (int c = lane * 4; c < H; c += 128) {
-    const float4 xv = *reinterpret_cast<const float4*>(row + c);
+    const float4 xv = *reinterpret_cast<const float4*>(row + emb_pad<H>(c));
     const float4 gv = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
     const float4 bv = __ldg(reinterpret_cast<const float4*>(p.beta + c));
     const float xx[4] = {xv.x, xv.y, xv.z, xv.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};

@@ -15,7 +15,8 @@ static cudaError_t embed_h(const EmbedParams& p, cudaStream_t st) {
     configured = dev;
   }
   constexpr int tok = EMB_THREADS / 32;
-  return launch_ex(embed_kernel<H>, dim3((p.T + tok - 1) / tok), dim3(EMB_THREADS), size_t(tok) * H * sizeof(float),
+  return launch_ex(embed_kernel<H>, dim3((p.T + tok - 1) / tok), dim3(EMB_THREADS),
+                   size_t(tok) * EmbLeaves<H>::ROW * sizeof(float),
                    st, 1, p);
 }
 

@@ -1,9 +1,27 @@
+#include "gemm_ln_persistent.cuh"
 #include "kernels.h"
 
 namespace samp {
 
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                        const EpiResLN::Params& p, cudaStream_t st) {
+  // Opt-in (SAMP_LN_PERSISTENT=1): persistent clusters with double-buffered TMEM when there
+  // are more row tiles than co-resident clusters (gemm_ln_persistent.cuh).  Bit-exact, but
+  // measured slower than one tile per CTA (C5 FFN2 1.80 vs 1.57 ms, C4 0.12 vs 0.11 ms:
+  // ncu shows SMs idle ~45% of the kernel), so not the default.
+  const int mtiles = (M + GEMM_BM - 1) / GEMM_BM;
+  if (std::getenv("SAMP_LN_PERSISTENT") != nullptr) {
+    switch (t.bn_ln * 10 + t.cluster_ln) {
+      case 1924:
+        if (mtiles > ln_persistent_clusters<KIND_I8, 192, 4, 4>())
+          return launch_gemm_ln_persistent<KIND_I8, 192, 4, 4>(a, b, M, kb, p, st);
+        break;
+      case 2564:
+        if (mtiles > ln_persistent_clusters<KIND_I8, 256, 3, 4>())
+          return launch_gemm_ln_persistent<KIND_I8, 256, 3, 4>(a, b, M, kb, p, st);
+        break;
+    }
+  }
   switch (t.bn_ln * 10 + t.cluster_ln) {
     case 1924: return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);

@@ -228,3 +228,32 @@ def test_packed_short_sequences_bit_exact(matcher):
     # same sequences one at a time (single-sequence tiles) give the same bits
     for s in (1, 3, 12):
         np.testing.assert_array_equal(eng.run(encs[s], plan).hidden_states, batch.sequence(s))
+
+
+# ---------------------------------------------------------------- large token counts
+@pytest.mark.parametrize("persistent", [False, True])
+@pytest.mark.parametrize("geom", ["base", "large"])
+def test_persistent_layernorm_gemms_bit_exact(geom, persistent, large_ner, monkeypatch):
+    """T > 37 x 128 tokens: one-tile LN GEMMs over many waves, and (SAMP_LN_PERSISTENT=1) the
+    persistent cluster GEMM (gemm_ln_persistent.cuh, st.async exchange of the LayerNorm
+    partials): both bit-exact with the oracle."""
+    if persistent:
+        monkeypatch.setenv("SAMP_LN_PERSISTENT", "1")
+    if geom == "large":
+        arch, model = large_ner
+        S, n = 256, 21                      # 5376 tokens
+    else:
+        arch = _archive(768, 12, 3072, "classification", 2, seed=5)
+        rng = np.random.default_rng(3)
+        model = _calibrate(arch, [(rng.integers(4, 1000, 64).tolist(), [0] * 64) for _ in range(2)])
+        S, n = 128, 44                      # 5632 tokens
+    eng = _engine(arch)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
+    rng = np.random.default_rng(31)
+    encs = [EncodedInput(rng.integers(4, 1000, S).tolist(), [0] * S, S - (s % 3) * 7) for s in range(n)]
+    batch = eng.run_batch(encs, plan)
+    for s in (0, 1, n // 2, n - 1):
+        enc = encs[s]
+        want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
+        np.testing.assert_array_equal(batch.sequence(s), want, err_msg=f"{geom} seq {s}")

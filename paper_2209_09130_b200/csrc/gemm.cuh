@@ -509,26 +509,32 @@ struct EpiF16Out {
 // (reference encoder.py:381-385 out-proj, :412-418 FFN2; kernels.layernorm :138-154)
 // Sum order: each thread reduces its (half) row = one numpy subtree; the two halves are
 // added (NE == 8), then the CLUSTER CTAs' partials in tree order through DSMEM.
-struct EpiResLN {
-  struct Params {
-    const float* bias;
-    const int8_t* res_i8;   // residual codes [M][H] (or null)
-    const float* res_f32;   // residual values [M][H] (or null)
-    float res_scale;
-    const float* gamma;
-    const float* beta;
-    float mult;             // int32 accumulator dequant multiplier
-    int acc_is_f32;         // kind::f16 GEMM: accumulator is already F32, no dequant
-    float eps;
-    int hidden;
-    int8_t* out_i8;  float s_out;   // optional
-    int deq_outputs;                // f32/f16 outputs carry F32(q)*s_out (MHA-only layers)
-    int f16_round;                  // reference fp16 storage: round the f32 output through f16
-    float* out_f32;                 // optional
-    __half* out_f16;                // optional
-    float* amax;                    // calibration: amax array (null = off)
-    int site, site2;                // sites tapped with the emitted values (site2 < 0: none)
-  };
+struct ResLNParams {
+  const float* bias;
+  const int8_t* res_i8;   // residual codes [M][H] (or null)
+  const float* res_f32;   // residual values [M][H] (or null)
+  float res_scale;
+  const float* gamma;
+  const float* beta;
+  float mult;             // int32 accumulator dequant multiplier
+  int acc_is_f32;         // kind::f16 GEMM: accumulator is already F32, no dequant
+  float eps;
+  int hidden;
+  int8_t* out_i8;  float s_out;   // optional
+  int deq_outputs;                // f32/f16 outputs carry F32(q)*s_out (MHA-only layers)
+  int f16_round;                  // reference fp16 storage: round the f32 output through f16
+  float* out_f32;                 // optional
+  __half* out_f16;                // optional
+  float* amax;                    // calibration: amax array (null = off)
+  int site, site2;                // sites tapped with the emitted values (site2 < 0: none)
+};
+// I8_ONLY: the hot INT8 chain (int8 residual, int32 accumulator, only int8 codes out):
+// the general variant's optional outputs are compiled out, shrinking the epilogue code
+// ~3x (ncu showed 20% "no_instruction" stalls on the 80 KB general kernel).
+template <bool I8_ONLY>
+struct EpiResLNT {
+  using Params = ResLNParams;
+
   // smem: [0,512) floats reduction scratch (per-half partials, 2 x CTA partials), then
   // bias / gamma / beta slices (BN floats each), then the int8 residual tile
   // [128][BN + 16] (16-byte row pad: conflict-free 16 B reads by consecutive rows)
@@ -664,11 +670,19 @@ struct EpiResLN {
 #pragma unroll
       for (int k = 0; k < NC / 32; ++k) {
         float res[32];
-        residual32<BN>(p, c, rtile, rbase, c.c0 + 32 * k, res);
+        if constexpr (I8_ONLY) {
+          const uint4* src = reinterpret_cast<const uint4*>(rtile + c.c0 + 32 * k);
+          const uint4 u0 = src[0], u1 = src[1];
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+          for (int j = 0; j < 32; ++j) res[j] = deq(int(int8_t((w[j / 4] >> (8 * (j % 4))) & 0xff)), p.res_scale);
+        } else {
+          residual32<BN>(p, c, rtile, rbase, c.c0 + 32 * k, res);
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const uint32_t u = r[32 * k + j];
-          const float acc = p.acc_is_f32 ? __uint_as_float(u) : __fmul_rn(__int2float_rn(int(u)), p.mult);
+          const float acc = !I8_ONLY && p.acc_is_f32 ? __uint_as_float(u) : __fmul_rn(__int2float_rn(int(u)), p.mult);
           x[32 * k + j] = __fadd_rn(__fadd_rn(acc, sbias[c.c0 + 32 * k + j]), res[j]);
         }
       }
@@ -706,10 +720,17 @@ struct EpiResLN {
           const int col = c.c0 + 32 * k + j;
           y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[32 * k + j], mean), inv), sgam[col]), sbet[col]);
         }
-        emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+        if constexpr (I8_ONLY) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = quant_pre_fast(y[j], rq);
+          store32_pre(p.out_i8 + rbase + c.n0 + c.c0 + 32 * k, v);
+        } else {
+          emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+        }
       }
     }
-    if (p.amax) {
+    if (!I8_ONLY && p.amax) {
       amax_commit(p.amax + p.site, amx);
       if (p.site2 >= 0) amax_commit(p.amax + p.site2, amx);
     }
@@ -872,6 +893,8 @@ struct EpiResLN {
     }
   }
 };
+using EpiResLN = EpiResLNT<false>;
+using EpiResLNI8 = EpiResLNT<true>;
 
 // ------------------------------------------------------------------ host launcher
 template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>

@@ -22,6 +22,15 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
         break;
     }
   }
+  // the hot chain (int8 residual in, int8 codes out, nothing else): compact epilogue
+  const bool i8_only = p.res_i8 && !p.acc_is_f32 && p.out_i8 && !p.deq_outputs && !p.f16_round && !p.amax &&
+                       !p.out_f32 && !p.out_f16;
+  if (i8_only) {
+    switch (t.bn_ln * 10 + t.cluster_ln) {
+      case 1924: return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
+      case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
+    }
+  }
   switch (t.bn_ln * 10 + t.cluster_ln) {
     case 1924: return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);

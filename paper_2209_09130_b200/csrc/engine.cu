@@ -117,6 +117,8 @@ struct Activations {
   int8_t *xq[2] = {nullptr, nullptr}, *qkv_i8 = nullptr, *ctx_i8 = nullptr, *ffn_in_i8 = nullptr, *mid_i8 = nullptr;
   int *ids = nullptr, *segs = nullptr, *pos = nullptr;
   float *logits = nullptr, *probs = nullptr, *pooled = nullptr;
+  int* idseg = nullptr;       // [2][cap]: per forward ids = idseg, segs = idseg + T (one H2D)
+  float* headbuf = nullptr;   // per forward logits [rows][L] | probs [rows][L] | labels [rows] (one D2H)
   int* labels = nullptr;
   // A-operand tensor maps (box 128 B x 128 rows) and attention maps (box one head row x 64 rows)
   CUtensorMap a_xq[2], a_ctx_i8, a_ffn_in, a_mid_i8, a_hid_f16, a_ctx_f16, a_ln1_f16, a_mid_f16;
@@ -173,6 +175,8 @@ struct samp_engine {
   std::map<std::string, std::pair<double, long>> prof;  // name -> (total ms, launches)
   int* pinned_ids = nullptr;   // staging for host inputs
   int pinned_cap = 0;
+  float* pinned_out = nullptr;  // staging for the head outputs (one D2H)
+  size_t pinned_out_cap = 0;
 };
 
 namespace samp {
@@ -199,7 +203,7 @@ static void ensure_activations(samp_engine* e, int T) {
   };
   drop(a.hid_f32); drop(a.ln1_f32); drop(a.hid_f16); drop(a.qkv_f16); drop(a.ctx_f16); drop(a.ln1_f16);
   drop(a.mid_f16); drop(a.xq[0]); drop(a.xq[1]); drop(a.qkv_i8); drop(a.ctx_i8); drop(a.ffn_in_i8);
-  drop(a.mid_i8); drop(a.ids); drop(a.segs); drop(a.pos); drop(a.logits); drop(a.probs); drop(a.labels); drop(a.pooled);
+  drop(a.mid_i8); drop(a.idseg); drop(a.pos); drop(a.headbuf); drop(a.pooled);
   a.hid_f32 = e->mem.alloc<float>(size_t(cap) * H);
   a.ln1_f32 = e->mem.alloc<float>(size_t(cap) * H);
   a.hid_f16 = e->mem.alloc<__half>(size_t(cap) * H);
@@ -213,12 +217,9 @@ static void ensure_activations(samp_engine* e, int T) {
   a.ctx_i8 = e->mem.alloc<int8_t>(size_t(cap) * H);
   a.ffn_in_i8 = e->mem.alloc<int8_t>(size_t(cap) * H);
   a.mid_i8 = e->mem.alloc<int8_t>(size_t(cap) * I);
-  a.ids = e->mem.alloc<int>(cap);
-  a.segs = e->mem.alloc<int>(cap);
+  a.idseg = e->mem.alloc<int>(2 * size_t(cap));
   a.pos = e->mem.alloc<int>(cap);
-  a.logits = e->mem.alloc<float>(size_t(cap) * L);
-  a.probs = e->mem.alloc<float>(size_t(cap) * L);
-  a.labels = e->mem.alloc<int>(cap);
+  a.headbuf = e->mem.alloc<float>(size_t(cap) * (2 * L + 1));
   a.pooled = e->mem.alloc<float>(size_t(POOL_KSPLIT) * cap * H);
   a.cap = cap;
   // GEMM A operands: K-major rows, 128-byte boxes, 128 rows
@@ -687,6 +688,7 @@ extern "C" void samp_engine_destroy(samp_engine* e) {
   cudaDeviceSynchronize();
   clear_graphs(e);
   if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
+  if (e->pinned_out) cudaFreeHost(e->pinned_out);
   cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -1005,18 +1007,25 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
     e->stages.clear();
     Activations& a = e->act;
     cudaStream_t st = e->stream_in_use;
+    const int nl = d.num_labels;
+    const size_t rows = head == SAMP_HEAD_CLASSIFY ? nseq : T;
+    a.ids = a.idseg;
+    a.segs = a.idseg + T;
+    a.logits = a.headbuf;
+    a.probs = a.headbuf + rows * nl;
+    a.labels = reinterpret_cast<int*>(a.headbuf + 2 * rows * nl);
     // ---------------- inputs
     if (io == SAMP_IO_HOST) {
       if (e->pinned_cap < 2 * T) {
         if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
+  if (e->pinned_out) cudaFreeHost(e->pinned_out);
         e->pinned_cap = std::max(2 * T, 8192);
         SAMP_CUDA(cudaMallocHost(&e->pinned_ids, size_t(e->pinned_cap) * sizeof(int)));
       }
       SAMP_CUDA(cudaStreamSynchronize(st));  // staging buffer reuse
       std::memcpy(e->pinned_ids, ids, size_t(T) * 4);
       std::memcpy(e->pinned_ids + T, segs, size_t(T) * 4);
-      SAMP_CUDA(cudaMemcpyAsync(a.ids, e->pinned_ids, size_t(T) * 4, cudaMemcpyHostToDevice, st));
-      SAMP_CUDA(cudaMemcpyAsync(a.segs, e->pinned_ids + T, size_t(T) * 4, cudaMemcpyHostToDevice, st));
+      SAMP_CUDA(cudaMemcpyAsync(a.ids, e->pinned_ids, size_t(T) * 8, cudaMemcpyHostToDevice, st));
     } else {
       SAMP_CUDA(cudaMemcpyAsync(a.ids, ids, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
       SAMP_CUDA(cudaMemcpyAsync(a.segs, segs, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
@@ -1058,17 +1067,29 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       enqueue_kernels(e, prec, nseq, head, st);
       if (graphable) e->seen.insert(key);
     }
-    const int nl = d.num_labels;
     const cudaMemcpyKind kind = io == SAMP_IO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    const size_t head_bytes = (2 * rows * nl + rows) * 4;
+    const bool staged = io == SAMP_IO_HOST && out && head != SAMP_HEAD_NONE && (out->logits || out->probs || out->labels);
     if (out) {
       if (out->hidden) SAMP_CUDA(cudaMemcpyAsync(out->hidden, a.hid_f32, size_t(T) * H * 4, kind, st));
-      const size_t rows = head == SAMP_HEAD_CLASSIFY ? nseq : T;
-      if (head != SAMP_HEAD_NONE) {
+      if (staged) {   // the three head outputs are contiguous on the device: one D2H
+        if (e->pinned_out_cap < head_bytes) {
+          if (e->pinned_out) cudaFreeHost(e->pinned_out);
+          e->pinned_out_cap = std::max<size_t>(head_bytes, 1 << 16);
+          SAMP_CUDA(cudaMallocHost(&e->pinned_out, e->pinned_out_cap));
+        }
+        SAMP_CUDA(cudaMemcpyAsync(e->pinned_out, a.headbuf, head_bytes, cudaMemcpyDeviceToHost, st));
+      } else if (head != SAMP_HEAD_NONE) {
         if (out->logits) SAMP_CUDA(cudaMemcpyAsync(out->logits, a.logits, rows * nl * 4, kind, st));
         if (out->probs) SAMP_CUDA(cudaMemcpyAsync(out->probs, a.probs, rows * nl * 4, kind, st));
         if (out->labels) SAMP_CUDA(cudaMemcpyAsync(out->labels, a.labels, rows * 4, kind, st));
       }
     }
     if (io == SAMP_IO_HOST) SAMP_CUDA(cudaStreamSynchronize(st));
+    if (staged) {
+      if (out->logits) std::memcpy(out->logits, e->pinned_out, rows * nl * 4);
+      if (out->probs) std::memcpy(out->probs, e->pinned_out + rows * nl, rows * nl * 4);
+      if (out->labels) std::memcpy(out->labels, e->pinned_out + 2 * rows * nl, rows * 4);
+    }
   });
 }

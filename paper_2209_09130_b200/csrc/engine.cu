@@ -81,6 +81,10 @@ static int pick_bn(int n) {
 constexpr int FFN1_BN[3] = {64, 96, 128};
 static int ffn1_bn_index(int T, int I, int slots, bool allow96 = true) {
   const int sms = slots;
+  if (const char* f = std::getenv("SAMP_FFN1_BN")) {   // measurement override
+    for (int k = 0; k < 3; ++k)
+      if (FFN1_BN[k] == std::atoi(f) && I % FFN1_BN[k] == 0) return k;
+  }
   const int mt = (T + GEMM_BM - 1) / GEMM_BM;
   int best = -1;
   long best_cost = 0;

@@ -130,6 +130,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    if constexpr (CLUSTER > 1) Epi::template cluster_init<BN>(epi_smem);
     fence_barrier_init();
   }
   if (warp == 0 && elect_one()) {
@@ -139,6 +140,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CLUSTER > 1) cluster_sync_all();   // peers' exchange barriers are initialised
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (warp == 0) {
@@ -206,7 +208,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (warp < GEMM_EPI_WARP0) {
     for (int i = 0; i < Epi::template cluster_barriers<CLUSTER>(); ++i) cluster_sync_all();
   }
-  if constexpr (CLUSTER > 1) cluster_sync_all();  // no CTA leaves while peers read its smem
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -540,10 +541,18 @@ struct EpiResLNT {
   // [128][BN + 16] (16-byte row pad: conflict-free 16 B reads by consecutive rows)
   static constexpr int RED_FLOATS = 4 * 128;
   template <int BN> __host__ __device__ static constexpr int res_ld() { return BN + 16; }
-  template <int BN> __host__ __device__ static constexpr int smem_bytes() {
-    return (RED_FLOATS + 3 * BN) * 4 + 128 * res_ld<BN>();
+  // cluster exchange (CLUSTER > 1): xpart [2 reductions][4][128] floats + xbar[2] mbarriers
+  template <int BN> __host__ __device__ static constexpr int xp_off() { return (RED_FLOATS + 3 * BN) * 4 + 128 * res_ld<BN>(); }
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return xp_off<BN>() + 2 * 4 * 128 * 4 + 16; }
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
+  // before the kernel's cluster-wide start barrier: the exchange barriers exist before any
+  // peer's st.async can complete on them
+  template <int BN>
+  __device__ static void cluster_init(uint8_t* smem) {
+    uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * 4 * 128 * 4);
+    mbar_init(&xb[0], 1);
+    mbar_init(&xb[1], 1);
   }
-  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return CLUSTER > 1 ? 2 : 0; }
   template <int BN>
   __device__ static void prefetch(const Params& p, uint8_t* smem, int m0, int n0, int M, int tid, int nt) {
     float* f = reinterpret_cast<float*>(smem) + RED_FLOATS;
@@ -563,24 +572,37 @@ struct EpiResLNT {
     }
   }
 
-  template <int CLUSTER, int NE>
-  __device__ static float reduce_row(float mine, const EpiCtx& c, float* halves, float* cta) {
+  // Row total of reduction `red` (0: sum, 1: sum of squares): the two column halves inside
+  // the CTA (NE == 8), then the CLUSTER CTAs' partials in rank order ((p0+p1)+(p2+p3)).
+  // The cluster exchange is push-based: every CTA st.async's its 128 row partials into each
+  // peer's xpart[red][rank][row], completing on the peer's xbar[red] (expect_tx of all
+  // CLUSTER*128 floats); nobody reads remote smem, so no cluster barrier is needed after
+  // the kernel's start (a CTA only exits after its own exchanges landed).
+  template <int BN, int CLUSTER, int NE>
+  __device__ static float reduce_row(float mine, const EpiCtx& c, float* halves, uint8_t* smem, int red) {
     float s = mine;
     if constexpr (NE == 8) {
-      halves[c.half * 128 + c.tile_row] = mine;
+      float* hv = halves + red * 256;   // one buffer per reduction: no reuse barrier
+      hv[c.half * 128 + c.tile_row] = mine;
       epi_bar_sync(c.ne_threads);
-      s = __fadd_rn(halves[c.tile_row], halves[128 + c.tile_row]);
+      s = __fadd_rn(hv[c.tile_row], hv[128 + c.tile_row]);
     }
     if constexpr (CLUSTER > 1) {
-      cta[c.tile_row] = s;      // both halves write the same value
-      cluster_sync_all();
+      float* xp = reinterpret_cast<float*>(smem + xp_off<BN>()) + red * 4 * 128;
+      uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * 4 * 128 * 4) + red;
+      if (c.ep_tid == 0) mbar_expect_tx(xb, CLUSTER * 128 * 4);
+      if (c.half == 0) {
+        const uint32_t me = cluster_rank();
+#pragma unroll
+        for (int rr = 0; rr < CLUSTER; ++rr)
+          st_async_f32(mapa_rank(xp + me * 128 + c.tile_row, rr), s, mapa_rank(xb, rr));
+      }
+      mbar_wait(xb, 0);
       float p[CLUSTER];
 #pragma unroll
-      for (int r = 0; r < CLUSTER; ++r) p[r] = dsmem_ld_f32(&cta[c.tile_row], r);
+      for (int r = 0; r < CLUSTER; ++r) p[r] = xp[r * 128 + c.tile_row];
       if constexpr (CLUSTER == 2) s = __fadd_rn(p[0], p[1]);
       else s = __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
-    } else if constexpr (NE == 8) {
-      epi_bar_sync(c.ne_threads);   // halves[] is reused by the second reduction
     }
     return s;
   }
@@ -652,8 +674,6 @@ struct EpiResLNT {
     constexpr int NC = BN / (NE / 4);
     static_assert(NC % 32 == 0 && NC <= 128, "one numpy leaf per thread");
     float* halves = reinterpret_cast<float*>(smem);
-    float* cta0 = halves + 256;
-    float* cta1 = cta0 + 128;
     const float* sbias = halves + RED_FLOATS;
     const float* sgam = sbias + BN;
     const float* sbet = sgam + BN;
@@ -700,13 +720,13 @@ struct EpiResLNT {
                        __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
     };
     const float hf = float(p.hidden);
-    const float total = reduce_row<CLUSTER, NE>(leaf([](float v) { return v; }), c, halves, cta0);
+    const float total = reduce_row<BN, CLUSTER, NE>(leaf([](float v) { return v; }), c, halves, smem, 0);
     const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
-    const float total2 = reduce_row<CLUSTER, NE>(leaf([mean](float v) {
+    const float total2 = reduce_row<BN, CLUSTER, NE>(leaf([mean](float v) {
                                                    const float d = __fsub_rn(v, mean);
                                                    return __fmul_rn(d, d);
                                                  }),
-                                                 c, halves, cta1);
+                                                 c, halves, smem, 1);
     const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
     const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);
@@ -749,8 +769,6 @@ struct EpiResLNT {
   template <int BN, int CLUSTER, int NE>
   __device__ static void run_tmem(const Params& p, const EpiCtx& c, uint8_t* smem) {
     float* halves = reinterpret_cast<float*>(smem);
-    float* cta0 = halves + 256;
-    float* cta1 = cta0 + 128;
     const float* sbias = halves + RED_FLOATS;
     const float* sgam = sbias + BN;
     const float* sbet = sgam + BN;
@@ -822,14 +840,14 @@ struct EpiResLNT {
       };
       return pairwise_sum(c.ncols, get8);
     };
-    const float total = reduce_row<CLUSTER, NE>(row_sum([](float x) { return x; }), c, halves, cta0);
+    const float total = reduce_row<BN, CLUSTER, NE>(row_sum([](float x) { return x; }), c, halves, smem, 0);
     const float hf = float(p.hidden);
     const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
-    const float total2 = reduce_row<CLUSTER, NE>(row_sum([mean](float x) {
+    const float total2 = reduce_row<BN, CLUSTER, NE>(row_sum([mean](float x) {
                                                    const float d = __fsub_rn(x, mean);
                                                    return __fmul_rn(d, d);
                                                  }),
-                                                 c, halves, cta1);
+                                                 c, halves, smem, 1);
     const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
     const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);

@@ -24,7 +24,11 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
       case 256: return launch_gemm_persistent<KIND_I8, 256, 4, NEP, Epi>(a, b, M, N, kb, p, st);
       case 128: return launch_gemm_persistent<KIND_I8, 128, 3, NEP, Epi, 2>(a, b, M, N, kb, p, st);
       case 96: return launch_gemm_persistent<KIND_I8, 96, 3, 8, Epi, 2>(a, b, M, N, kb, p, st);
+#ifdef SAMP_FFN1_64X3
+      case 64: return launch_gemm_persistent<KIND_I8, 64, 2, 8, Epi, 3>(a, b, M, N, kb, p, st);
+#else
       case 64: return launch_gemm_persistent<KIND_I8, 64, 4, 8, Epi, 2>(a, b, M, N, kb, p, st);
+#endif
     }
     return cudaErrorInvalidValue;
   }

@@ -29,19 +29,6 @@
 
 namespace samp {
 
-__device__ __forceinline__ uint32_t mapa_rank(const void* local, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_addr(local)), "r"(rank));
-  return remote;
-}
-// asynchronous remote store whose completion is a complete_tx on the destination CTA's
-// mbarrier (data and barrier live in the same CTA: no cluster-scope fence, which would
-// compile to MEMBAR.ALL.GPU + L1 invalidation and measured 1.5x slower per tile)
-__device__ __forceinline__ void st_async_f32(uint32_t remote, float v, uint32_t remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
-               :: "r"(remote), "r"(__float_as_uint(v)), "r"(remote_bar) : "memory");
-}
-
 template <int BN, int STAGES, int CLUSTER>
 struct LnPersistLayout {
   static constexpr int A_BYTES = GEMM_BM * 128;

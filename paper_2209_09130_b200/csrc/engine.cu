@@ -66,6 +66,7 @@ struct LayerDev {
   double s_w[6] = {0, 0, 0, 0, 0, 0};  // qw kw vw ow w1 w2
   double b1_absmax = 0;                 // max|b1|: bounds the FFN1 GELU argument
   CUtensorMap m_qkv_i8, m_wo_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w2_f16;
+  CUtensorMap m_wo_i8_64, m_w2_i8_64;    // 64-row boxes: split-K GEMMs for small batches
   CUtensorMap m_w1_i8[3], m_w1_f16[3];   // FFN1 B operand, box rows FFN1_BN[k]
 };
 
@@ -122,6 +123,7 @@ struct Activations {
   int *ids = nullptr, *segs = nullptr, *pos = nullptr;
   float *logits = nullptr, *probs = nullptr, *pooled = nullptr;
   int* idseg = nullptr;       // [2][cap]: per forward ids = idseg, segs = idseg + T (one H2D)
+  int* ws = nullptr;          // [cap][H] int32 split-K accumulators (zero between uses)
   float* headbuf = nullptr;   // per forward logits [rows][L] | probs [rows][L] | labels [rows] (one D2H)
   int* labels = nullptr;
   // A-operand tensor maps (box 128 B x 128 rows) and attention maps (box one head row x 64 rows)
@@ -207,7 +209,7 @@ static void ensure_activations(samp_engine* e, int T) {
   };
   drop(a.hid_f32); drop(a.ln1_f32); drop(a.hid_f16); drop(a.qkv_f16); drop(a.ctx_f16); drop(a.ln1_f16);
   drop(a.mid_f16); drop(a.xq[0]); drop(a.xq[1]); drop(a.qkv_i8); drop(a.ctx_i8); drop(a.ffn_in_i8);
-  drop(a.mid_i8); drop(a.idseg); drop(a.pos); drop(a.headbuf); drop(a.pooled);
+  drop(a.mid_i8); drop(a.idseg); drop(a.pos); drop(a.headbuf); drop(a.pooled); drop(a.ws);
   a.hid_f32 = e->mem.alloc<float>(size_t(cap) * H);
   a.ln1_f32 = e->mem.alloc<float>(size_t(cap) * H);
   a.hid_f16 = e->mem.alloc<__half>(size_t(cap) * H);
@@ -222,6 +224,8 @@ static void ensure_activations(samp_engine* e, int T) {
   a.ffn_in_i8 = e->mem.alloc<int8_t>(size_t(cap) * H);
   a.mid_i8 = e->mem.alloc<int8_t>(size_t(cap) * I);
   a.idseg = e->mem.alloc<int>(2 * size_t(cap));
+  a.ws = e->mem.alloc<int>(size_t(cap) * H);
+  SAMP_CUDA(cudaMemset(a.ws, 0, size_t(cap) * H * sizeof(int)));
   a.pos = e->mem.alloc<int>(cap);
   a.headbuf = e->mem.alloc<float>(size_t(cap) * (2 * L + 1));
   a.pooled = e->mem.alloc<float>(size_t(POOL_KSPLIT) * cap * H);
@@ -426,6 +430,37 @@ static void gelu_fast_prepare(samp_engine* e, const uint8_t* prec) {
   }
 }
 
+// Small batches: the out-projection / FFN2 as a split-K GEMM into the int32 workspace
+// (64-wide tiles, grid z = ksplit k-block groups) + the row LayerNorm kernel, instead of
+// a handful of 4-CTA clusters each streaming the whole K.  Returns false (caller runs the
+// fused kernel) unless the launch is the hot int8 chain and the batch is small enough.
+// Opt-in (SAMP_SPLITK=1): bit-exact, but the extra row-LayerNorm launch cancels the GEMM
+// gain at batch 1 (fully-quant p50 0.595 vs 0.575 ms), so the fused cluster kernel stays
+// the default.
+static int splitk_factor(int T, int N, int kblocks, int sms) {
+  if (!std::getenv("SAMP_SPLITK")) return 0;
+  const int tiles = ((T + GEMM_BM - 1) / GEMM_BM) * (N / 64);
+  int best = 0;
+  for (int d = 2; d <= kblocks; ++d)
+    if (kblocks % d == 0 && tiles * d <= sms + sms / 4) best = d;
+  return best;
+}
+static bool ln_gemm_splitk(samp_engine* e, const char* name, const CUtensorMap& a_map, const CUtensorMap& b64,
+                           int K, const EpiResLN::Params& lp, cudaStream_t st) {
+  const int T = e->geo.T, H = e->d.hidden;
+  const bool i8_only = lp.res_i8 && !lp.acc_is_f32 && lp.out_i8 && !lp.deq_outputs && !lp.f16_round && !lp.amax &&
+                       !lp.out_f32 && !lp.out_f16;
+  if (!i8_only || !ln_rows_supported(H) || H % 64) return false;
+  const int ks = splitk_factor(T, H, K / 128, e->sms);
+  if (ks < 2) return false;
+  EpiSplitKAdd::Params sp{e->act.ws, H};
+  check_launch(e, gemm_splitk_i8(a_map, b64, T, H, K, ks, sp, st), name);
+  LnRowsParams rp{e->act.ws, lp.res_i8, lp.res_scale, lp.bias, lp.gamma, lp.beta, lp.mult, lp.eps, T,
+                  lp.out_i8, lp.s_out};
+  check_launch(e, launch_ln_rows(rp, H, st), "ln_rows");
+  return true;
+}
+
 // one encoder layer; `in_q` = index of xq holding this layer's input codes (INT8 inputs)
 static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   const int L = e->d.num_layers, H = e->d.hidden, I = e->d.intermediate, T = e->geo.T;
@@ -490,7 +525,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.out_f32 = a.ln1_f32;
       lp.out_f16 = a.ln1_f16;
     }
-    check_launch(e, gemm_ln_i8(t, a.a_ctx_i8, w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
+    if (!ln_gemm_splitk(e, "outproj_i8", a.a_ctx_i8, w.m_wo_i8_64, H, lp, st))
+      check_launch(e, gemm_ln_i8(t, a.a_ctx_i8, w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
     record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
   } else {
     record(e, "in_f32", i, a.hid_f32, size_t(T) * H * 4);
@@ -568,7 +604,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.res_i8 = a.ffn_in_i8;
     lp.res_scale = f32(s_fin);
     lp.mult = mult_of(s_mid, w.s_w[5]);
-    check_launch(e, gemm_ln_i8(t, a.a_mid_i8, w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
+    if (!ln_gemm_splitk(e, "ffn2_i8", a.a_mid_i8, w.m_w2_i8_64, I, lp, st))
+      check_launch(e, gemm_ln_i8(t, a.a_mid_i8, w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
   } else {
     EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
     const int k1 = ffn1_bn_index(T, I, e->sms, false);   // EpiF16Out walks 32-column chunks
@@ -768,12 +805,14 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     const Tiles& tl = e->tiles;
     w.m_qkv_i8 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, tl.bn_qkv);
     w.m_wo_i8 = tmap_i8(w.wo_i8, H, H, H, 128, tl.bn_ln);
+    w.m_wo_i8_64 = tmap_i8(w.wo_i8, H, H, H, 128, 64);
     for (int k = 0; k < 3; ++k)
       if (I % FFN1_BN[k] == 0) {
         w.m_w1_i8[k] = tmap_i8(w.w1_i8, I, H, H, 128, FFN1_BN[k]);
         w.m_w1_f16[k] = tmap_f16(w.w1_f16, I, H, H, 64, FFN1_BN[k]);
       }
     w.m_w2_i8 = tmap_i8(w.w2_i8, H, I, I, 128, tl.bn_ln);
+    w.m_w2_i8_64 = tmap_i8(w.w2_i8, H, I, I, 128, 64);
     w.m_qkv_f16 = tmap_f16(w.qkv_f16, 3 * H, H, H, 64, tl.bn_qkv);
     w.m_wo_f16 = tmap_f16(w.wo_f16, H, H, H, 64, tl.bn_ln);
     w.m_w2_f16 = tmap_f16(w.w2_f16, H, I, I, 64, tl.bn_ln);

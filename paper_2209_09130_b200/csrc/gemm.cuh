@@ -116,7 +116,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const uint32_t warp = warp_id();
   const int m0 = blockIdx.y * GEMM_BM;
   const int n0 = blockIdx.x * BN;
-  const int nk = k_bytes / 128;
+  // split-K (gridDim.z > 1, host guarantees z | k-blocks): this CTA's k-block range
+  const int nk = k_bytes / 128 / int(gridDim.z);
+  const int kb0 = int(blockIdx.z) * nk;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
   unsigned long long* stamp = stamps && cta < GEMM_STAMP_CTAS ? stamps + size_t(cta) * GEMM_STAMPS : nullptr;
   if (stamp && threadIdx.x == 0) {
@@ -146,7 +148,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (warp == 0) {
     if (elect_one()) {
       // coordinates are in elements: 128 bytes of K = 128 int8 or 64 f16
-      auto kcol = [](int kb) { return KIND == KIND_I8 ? kb * 128 : kb * 64; };
+      auto kcol = [kb0](int kb) { return KIND == KIND_I8 ? (kb0 + kb) * 128 : (kb0 + kb) * 64; };
       // weights (B) do not depend on the previous kernel: fill the ring's B halves
       // while it drains, then wait for it and stream A
       const int pre = nk < STAGES ? nk : STAGES;
@@ -285,6 +287,42 @@ struct EpiStoreAcc {
 #pragma unroll
         for (int j = 0; j < 8; ++j) dst[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
       }
+    }
+  }
+};
+
+// Split-K partial: the int32 accumulator tile is added into an int32 workspace with
+// coalesced red.global.add (the tile is transposed through smem so a warp's 32 lanes hit
+// 32 consecutive columns).  Integer addition is exact and order-independent, so the
+// workspace holds exactly the full-K accumulator whatever the CTA order.  The consumer
+// (ln_rows_kernel) re-zeroes the workspace rows it reads.
+struct EpiSplitKAdd {
+  struct Params {
+    int* ws;     // [M][ldw]
+    int ldw;
+  };
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return 128 * (BN + 1) * 4; }
+  template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
+  template <int BN> __device__ static void prefetch(const Params&, uint8_t*, int, int, int, int, int) {}
+  template <int BN, int CLUSTER, int NE>
+  __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    int* tile = reinterpret_cast<int*>(smem);   // [128][BN + 1]
+#pragma unroll 1
+    for (int col = 0; col < c.ncols; col += 32) {
+      uint32_t r[32];
+      tmem_ld32(c.taddr + col, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) tile[c.tile_row * (BN + 1) + c.c0 + col + j] = int(r[j]);
+    }
+    epi_bar_sync(c.ne_threads);
+    const int lane = c.ep_tid & 31, w = c.ep_tid >> 5, nw = c.ne_threads >> 5;
+    for (int row = w; row < 128; row += nw) {
+      const int m0 = c.row - c.tile_row;
+      if (m0 + row >= c.M) break;
+      int* dst = p.ws + size_t(m0 + row) * p.ldw + c.n0;
+      for (int cc = lane; cc < BN; cc += 32)
+        asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" :: "l"(dst + cc), "r"(tile[row * (BN + 1) + cc]) : "memory");
     }
   }
 };
@@ -917,7 +955,7 @@ using EpiResLNI8 = EpiResLNT<true>;
 // ------------------------------------------------------------------ host launcher
 template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
 inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N, int k_bytes,
-                               const typename Epi::Params& p, cudaStream_t stream) {
+                               const typename Epi::Params& p, cudaStream_t stream, int ksplit = 1) {
   using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
   auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi>;
   static thread_local int configured_device = -1;
@@ -929,7 +967,7 @@ inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_
     configured_device = dev;
   }
   unsigned long long* stamps = g_gemm_stamps;
-  return launch_ex(kern, dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, 1), dim3(64 + 32 * NE, 1, 1), Lay::TOTAL, stream,
+  return launch_ex(kern, dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, ksplit), dim3(64 + 32 * NE, 1, 1), Lay::TOTAL, stream,
                    CLUSTER, map_a, map_b, M, k_bytes, p, stamps);
 }
 

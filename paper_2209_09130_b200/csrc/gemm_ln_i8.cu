@@ -43,4 +43,9 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
   return cudaErrorInvalidValue;
 }
 
+cudaError_t gemm_splitk_i8(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb, int ksplit,
+                           const EpiSplitKAdd::Params& p, cudaStream_t st) {
+  return launch_gemm<KIND_I8, 64, 4, 1, 4, EpiSplitKAdd>(a, b, M, N, kb, p, st, ksplit);
+}
+
 }  // namespace samp

@@ -7,6 +7,7 @@
 #include "embed.cuh"
 #include "gemm.cuh"
 #include "heads.cuh"
+#include "ln_rows.cuh"
 
 namespace samp {
 
@@ -25,6 +26,9 @@ cudaError_t gemm_gelu_i8(int bn, int mode, const CUtensorMap& a, const CUtensorM
 // gemm_ln.cu
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                        const EpiResLN::Params& p, cudaStream_t st);
+// small batches: split-K GEMM into an int32 workspace (64-wide tiles, grid z = ksplit)
+cudaError_t gemm_splitk_i8(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb, int ksplit,
+                           const EpiSplitKAdd::Params& p, cudaStream_t st);
 cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                         const EpiResLN::Params& p, cudaStream_t st);
 // gemm_f16.cu
@@ -37,6 +41,8 @@ cudaError_t launch_attention_f16(const CUtensorMap& map, const AttnParams& p, in
                                  cudaStream_t st);
 // misc_kernels.cu
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st);
+cudaError_t launch_ln_rows(const LnRowsParams& p, int hidden, cudaStream_t st);
+bool ln_rows_supported(int hidden);
 cudaError_t launch_classify(const HeadParams& p, cudaStream_t st);
 cudaError_t launch_tag(const HeadParams& p, cudaStream_t st);
 cudaError_t launch_pack_weight(const float* w, int K, int N, float scale, int8_t* out_i8, __half* out_f16,

@@ -20,6 +20,27 @@ static cudaError_t embed_h(const EmbedParams& p, cudaStream_t st) {
                    st, 1, p);
 }
 
+template <int H>
+static cudaError_t ln_rows_h(const LnRowsParams& p, cudaStream_t st) {
+  constexpr int rows = LNR_THREADS / 32;
+  return launch_ex(ln_rows_kernel<H>, dim3((p.M + rows - 1) / rows), dim3(LNR_THREADS),
+                   size_t(rows) * EmbLeaves<H>::ROW * sizeof(float), st, 1, p);
+}
+
+bool ln_rows_supported(int hidden) {
+  return hidden == 768 || hidden == 1024 || hidden == 512 || hidden == 384;
+}
+
+cudaError_t launch_ln_rows(const LnRowsParams& p, int hidden, cudaStream_t st) {
+  switch (hidden) {
+    case 384: return ln_rows_h<384>(p, st);
+    case 512: return ln_rows_h<512>(p, st);
+    case 768: return ln_rows_h<768>(p, st);
+    case 1024: return ln_rows_h<1024>(p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st) {
   switch (p.hidden) {
     case 64: return embed_h<64>(p, st);

@@ -257,3 +257,31 @@ def test_persistent_layernorm_gemms_bit_exact(geom, persistent, large_ner, monke
         enc = encs[s]
         want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
         np.testing.assert_array_equal(batch.sequence(s), want, err_msg=f"{geom} seq {s}")
+
+
+# ---------------------------------------------------------------- small batches: split-K
+@pytest.mark.parametrize("lens", [[128], [100, 77], [40, 200, 60]])
+def test_small_batch_splitk_layernorm_bit_exact(lens, monkeypatch):
+    """T <= a few row tiles: out-projection / FFN2 run as split-K GEMMs into an int32
+    workspace + the row LayerNorm kernel (ln_rows.cuh).  Bit-exact with the oracle and with
+    the fused cluster kernel (default; the split-K path is opt-in, SAMP_SPLITK=1)."""
+    monkeypatch.setenv("SAMP_SPLITK", "1")
+    arch = _archive(768, 12, 3072, "classification", 2, seed=5)
+    rng = np.random.default_rng(3)
+    model = _calibrate(arch, [(rng.integers(4, 1000, 64).tolist(), [0] * 64) for _ in range(2)])
+    eng = _engine(arch)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
+    rng = np.random.default_rng(41)
+    encs = [EncodedInput(rng.integers(4, 1000, n).tolist(), [0] * n, n - 3) for n in lens]
+    split = eng.run_batch(encs, plan)
+    for s, enc in enumerate(encs):
+        want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
+        np.testing.assert_array_equal(split.sequence(s), want, err_msg=f"seq {s}")
+    monkeypatch.delenv("SAMP_SPLITK")
+    eng2 = _engine(arch)
+    fused = eng2.run_batch(encs, plan)
+    np.testing.assert_array_equal(split.hidden_states, fused.hidden_states)
+    # repeated calls (CUDA-graph replay) keep the workspace clean
+    for _ in range(3):
+        np.testing.assert_array_equal(eng.run_batch(encs, plan).hidden_states, split.hidden_states)

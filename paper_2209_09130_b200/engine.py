@@ -120,7 +120,13 @@ class Engine:
 
     def _push_calibration(self) -> None:
         table = self.archive.calibration
+        # fast path: the very table object pushed last (held, so its id cannot be reused),
+        # unchanged through its API (version) and with the same entry count
+        key = None if table is None else (table.version, len(table.entries))
+        if table is not None and table is getattr(self, "_pushed_table", None) and key == self._pushed_key:
+            return
         state = None if table is None else tuple(sorted((s, e.amax) for s, e in table.entries.items()))
+        self._pushed_table, self._pushed_key = table, key
         if state == self._pushed_calibration:
             return
         _lib.check(self._lib.samp_clear_calibration(self._h))

@@ -169,8 +169,16 @@ def run_samp(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # one rank per GPU over NCCL; SAMP_BENCH_BACKEND=gloo lets several ranks share a GPU
+    # (functional test of the multi-rank path on a 1-GPU box)
+    backend = os.environ.get("SAMP_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -244,7 +252,7 @@ def run_samp(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -338,7 +346,10 @@ def run_samp(args):
 
     line = None
     if rank == 0:
-        cpu = cpu_baseline(arch, plan, args, wl=wl) if (world == 1 and not args.no_cpu) else None
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            with _all_host_threads():
+                cpu = cpu_baseline(arch, plan, args, wl=wl)
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "sentences/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
@@ -357,6 +368,24 @@ def run_samp(args):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _all_host_threads():
+    """BLAS thread pools sized to every host core this process may use (torchrun sets
+    OMP_NUM_THREADS=1 per rank; the reference arm runs on rank 0 alone and gets them all)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=_host_cores())
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
 
 
 def _blas_threads():
@@ -405,15 +434,17 @@ def run_reference(args):
     L = arch.manifest.num_layers
     plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
     n = args.ref_sentences
-    for _ in range(args.warmup):
-        cpu_baseline(arch, plan, args, n_sent=1)
     vals = []
     t_all = 0.0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        r = cpu_baseline(arch, plan, args, n_sent=n)
-        t_all += time.perf_counter() - t0
-        vals.append(r["value"])
+    with _all_host_threads():
+        for _ in range(args.warmup):
+            cpu_baseline(arch, plan, args, n_sent=1)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = cpu_baseline(arch, plan, args, n_sent=n)
+            t_all += time.perf_counter() - t0
+            vals.append(r["value"])
+        cores = _blas_threads()
     value = n * args.steps / t_all
     line = {
         "metric": METRIC, "impl": "reference", "value": round(value, 4), "unit": "sentences/s",
@@ -422,7 +453,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "int8", "data": "synthetic",
         "config": {"workload": "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 (configs[1])",
                    "model": MODEL, "plan": "FULLY_QUANT k=12", "step_sample": f"{n} sentences of the batch"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "sentences/s", "cores": _blas_threads(),
+        "cpu_baseline": {"value": round(value, 4), "unit": "sentences/s", "cores": cores,
                          "kind": "port", "sample": f"{n} x 128-token sentences per step"},
         "e2e": {"value": round(value, 4), "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

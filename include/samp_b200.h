@@ -126,6 +126,21 @@ int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, siz
 int samp_debug_gemm_i8(const int8_t* a, const int8_t* b, int32_t* c, int m, int n, int k);
 int samp_debug_gemm_f16(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);
 
+/* Native multi-threaded host tokenizer (the paper's C++ tokenizer feeding the packed
+ * varlen batch; replaces the reference's per-text tokenization.encode loop, cli.py:375-377,
+ * SPEC.md:230-286).  tokens[i] is the UTF-8 token of id i.  Returns NULL when a special
+ * token is missing or max_seq_len < 3 (callers use the Python encoder then). */
+typedef struct samp_tokenizer samp_tokenizer;
+samp_tokenizer* samp_tokenizer_create(const char* const* tokens, int ntokens, int do_lower_case, int max_seq_len,
+                                      int char_mode);
+void samp_tokenizer_destroy(samp_tokenizer* tok);
+/* Encode n texts (text_b NULL or per-item NULL for single texts) into padded rows
+ * ids/segs[n][max_seq_len], att[n] on nthreads threads.  Items with non-ASCII bytes are
+ * flagged fallback[i] = 1 and left to the caller (Unicode normalisation); returns their
+ * count. */
+int samp_tokenize_batch(samp_tokenizer* tok, const char* const* text_a, const char* const* text_b, int n,
+                        int nthreads, int32_t* ids, int32_t* segs, int32_t* att, uint8_t* fallback);
+
 /* numerics validation: exhaustive (all 2^32 inputs) comparisons of the branch-free
  * quantize / divide / exp used by the kernels against their IEEE-divide formulations,
  * and device evaluation of fn 0 = numpy exp, 1 = numpy (SVML) tanh, 2 = reference GELU */

@@ -73,6 +73,12 @@ SIGNATURES = [
     ("samp_debug_div_exhaustive", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_exp_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_gelu_finite_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
+    ("samp_tokenizer_create", ctypes.c_void_p, [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int]),
+    ("samp_tokenizer_destroy", None, [ctypes.c_void_p]),
+    ("samp_tokenize_batch", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
+                                           ctypes.POINTER(ctypes.c_char_p), ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("samp_debug_exp2_fast_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_gelu_fast_check", ctypes.c_int, [ctypes.c_float, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_unary", ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long]),

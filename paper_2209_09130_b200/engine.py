@@ -258,6 +258,21 @@ class Engine:
                     "kind": self._head_kind(), "archive": id(self.archive)}
         return EncoderOutput(hidden_states=res.hidden_states, taps=None, head=head)
 
+    def encode_batch(self, texts_a, texts_b=None, threads: int | None = None):
+        """Tokenize many texts at once on the native multi-threaded tokenizer (rows padded
+        to the vocab's max_seq_len, as encode_text).  Returns packed (seq_start, att_len,
+        ids, segs) for forward_packed."""
+        from .tokenization import encode_batch
+        ids, segs, att = encode_batch(self.vocab, texts_a, texts_b, threads)
+        n, L = ids.shape
+        seq_start = (np.arange(n + 1, dtype=np.int32) * L).astype(np.int32)
+        return seq_start, att, ids.reshape(-1), segs.reshape(-1)
+
+    def run_texts(self, plan: PrecisionPlan, texts_a, texts_b=None, hidden: bool = False,
+                  head: int | None = None) -> BatchOutput:
+        """Raw text -> device head results in one call: native tokenizer + one forward."""
+        return self.forward_packed(plan, *self.encode_batch(texts_a, texts_b), hidden=hidden, head=head)
+
     def run_batch(self, encs, plan: PrecisionPlan, hidden: bool = True, head: int | None = None) -> BatchOutput:
         """Batched, padding-free Engine.run over many EncodedInputs (one device call)."""
         for e in encs:

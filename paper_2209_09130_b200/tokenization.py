@@ -13,8 +13,13 @@ which requires identical token ids for the sample texts.
 
 from __future__ import annotations
 
+import ctypes
+import os
 import unicodedata
+import weakref
 from dataclasses import dataclass
+
+import numpy as np
 
 from .errors import ConfigurationError
 
@@ -206,3 +211,57 @@ def encode(vocab: Vocab, text_a: str, text_b: str | None = None) -> EncodedInput
     ids = ids + [vocab.pad_id] * pad
     segs = segs + [segs[-1] if text_b is not None else 0] * pad
     return EncodedInput(ids, segs, length)
+
+
+# ------------------------------------------------------------------ native batch encoder
+def _native_tokenizer(vocab: Vocab):
+    """The library's tokenizer for this vocab (built once per Vocab, freed with it)."""
+    h = getattr(vocab, "_native", None)
+    if h is not None:
+        return h
+    from . import _lib
+    lib = _lib.load()
+    toks = [vocab.id_to_token[i].encode("utf-8") for i in range(len(vocab))]
+    arr = (ctypes.c_char_p * len(toks))(*toks)
+    h = lib.samp_tokenizer_create(arr, len(toks), int(vocab.do_lower_case), vocab.max_seq_len, int(vocab.char_mode))
+    if h:
+        weakref.finalize(vocab, lib.samp_tokenizer_destroy, h)
+    vocab._native = h or 0
+    return vocab._native
+
+
+def encode_batch(vocab: Vocab, texts_a, texts_b=None, threads: int | None = None):
+    """encode() over many texts at once on the native multi-threaded tokenizer.
+
+    Returns (ids, segs, att): int32 [n][max_seq_len], [n][max_seq_len], [n] — row i equals
+    encode(vocab, texts_a[i], texts_b[i]).  Texts with non-ASCII characters are encoded by
+    the Python path (Unicode normalisation), everything else natively.
+    """
+    texts_a = list(texts_a)
+    n = len(texts_a)
+    if texts_b is not None:
+        texts_b = list(texts_b)
+        if len(texts_b) != n:
+            raise ConfigurationError("texts_a and texts_b differ in length")
+    L = vocab.max_seq_len
+    ids = np.empty((n, L), np.int32)
+    segs = np.empty((n, L), np.int32)
+    att = np.empty(n, np.int32)
+    fb = np.ones(n, np.uint8)
+    h = _native_tokenizer(vocab) if n else 0
+    if h:
+        from . import _lib
+        def cstr(t):   # an embedded NUL would truncate the C string: route it to Python
+            b = t.encode("utf-8")
+            return b"\x80" if b"\x00" in b else b
+        a_arr = (ctypes.c_char_p * n)(*[cstr(t) for t in texts_a])
+        b_arr = None
+        if texts_b is not None:
+            b_arr = (ctypes.c_char_p * n)(*[None if t is None else cstr(t) for t in texts_b])
+        nthreads = threads or min(16, os.cpu_count() or 1)
+        _lib.load().samp_tokenize_batch(h, a_arr, b_arr, n, nthreads, ids.ctypes.data, segs.ctypes.data,
+                                        att.ctypes.data, fb.ctypes.data)
+    for i in np.nonzero(fb)[0]:
+        enc = encode(vocab, texts_a[i], None if texts_b is None else texts_b[i])
+        ids[i], segs[i], att[i] = enc.token_ids, enc.segment_ids, enc.attention_length
+    return ids, segs, att

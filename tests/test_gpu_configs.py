@@ -285,3 +285,22 @@ def test_small_batch_splitk_layernorm_bit_exact(lens, monkeypatch):
     # repeated calls (CUDA-graph replay) keep the workspace clean
     for _ in range(3):
         np.testing.assert_array_equal(eng.run_batch(encs, plan).hidden_states, split.hidden_states)
+
+
+# ---------------------------------------------------------------- raw text in one call
+def test_run_texts_equals_encoded_runs(matcher):
+    """Engine.run_texts (native tokenizer + packed forward) == per-text encode_text + run."""
+    arch, _ = matcher
+    eng = _engine(arch)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FFN_ONLY", L, L)
+    words = ["w%d" % i for i in range(4, 300)]
+    rng = np.random.default_rng(5)
+    a = [" ".join(rng.choice(words, size=int(rng.integers(3, 40)))) for _ in range(12)]
+    b = [" ".join(rng.choice(words, size=int(rng.integers(3, 40)))) for _ in range(12)]
+    res = eng.run_texts(plan, a, b, hidden=True)
+    for i in range(len(a)):
+        enc = eng.encode_text(a[i], b[i])
+        one = eng.run(enc, plan)
+        np.testing.assert_array_equal(res.sequence(i), one.hidden_states)
+        np.testing.assert_array_equal(res.logits[i], one.head["logits"][0])

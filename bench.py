@@ -284,6 +284,30 @@ def run_samp(args):
            "h2d_bytes_per_step": int(ids.nbytes + segs.nbytes),
            "d2h_bytes_per_step": int(rows * nl * 4 * 2 + rows * 4)}
 
+    # ---------------- raw text end to end: native tokenizer + forward (extra information)
+    e2e_text = None
+    if not wl.pairs:
+        from paper_2209_09130_b200.tokenization import Vocab, encode_batch
+        v = arch.vocab
+        vs = Vocab(v.token_to_id, do_lower_case=v.do_lower_case, max_seq_len=SEQ)
+        words = [t for t in v.token_to_id if t.isalpha() and t.islower()]
+        trng = np.random.default_rng(7)
+        texts = [" ".join(trng.choice(words, size=SEQ - 2)) for _ in range(BATCH)]
+        t_tot = 0.0
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tids, tsegs, tatt = encode_batch(vs, texts)
+            tstart = (np.arange(BATCH + 1) * SEQ).astype(np.int32)
+            eng.forward_packed(plan, tstart, tatt, tids.reshape(-1), tsegs.reshape(-1), hidden=False)
+            if i >= args.warmup:
+                t_tot += time.perf_counter() - t0
+        t_tot = max_over_ranks(t_tot)
+        e2e_text = {"value": round(world * BATCH * args.steps / t_tot, 1), "unit": "sentences/s",
+                    "input": f"{BATCH} raw texts of {SEQ - 2} vocabulary words per GPU per step",
+                    "tokenizer": "native multi-threaded (samp_tokenize_batch)"}
+
     # ---------------- per-kernel device times (separate pass, CUDA events per launch)
     _lib.check(lib.samp_set_profiling(eng.handle, 1))
     timed_steps(args.steps, fwd)
@@ -360,7 +384,7 @@ def run_samp(args):
                        "l2": "flushed before every timed step (256 MiB write)",
                        "calibration": "reference (tests/golden)" if wl.key == "c2" else "on-device, 8 rng(1) sequences"},
             "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
-            "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps, "e2e_text": e2e_text,
             "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels,
         }
         print(json.dumps(line), flush=True)

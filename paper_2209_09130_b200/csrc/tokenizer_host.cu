@@ -11,8 +11,11 @@
 // Inputs containing any non-ASCII byte are not tokenized here: they are flagged and the
 // caller runs the Python path for them (Unicode normalisation / categories), so results
 // are identical for every input.
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <string_view>
 #include <thread>
@@ -21,11 +24,73 @@
 
 namespace {
 
+// Persistent workers (thread creation costs ~50-300 us, more than a small batch's work)
+class Pool {
+ public:
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  // run fn(tid) for tid in [0, n) on n-1 workers + the caller; returns when all are done
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> call(call_);   // one batch at a time per tokenizer
+    while (int(threads_.size()) < n - 1) {
+      const int id = int(threads_.size()) + 1;
+      threads_.emplace_back([this, id] { loop(id); });
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      active_ = n;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int id) {
+    unsigned long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* fn;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (id >= active_) continue;
+        fn = fn_;
+      }
+      (*fn)(id);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex m_, call_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int active_ = 0, pending_ = 0;
+  unsigned long gen_ = 0;
+  bool stop_ = false;
+};
+
 struct Tokenizer {
   std::unordered_map<std::string, int> ids;
   bool lower = true, char_mode = false;
   int max_len = 128;
   int cls = 0, sep = 0, pad = 0, unk = 0;
+  Pool pool;
 };
 
 bool ascii_only(const char* s) {
@@ -176,7 +241,7 @@ int samp_tokenize_batch(samp_tokenizer* h, const char* const* text_a, const char
                         int32_t* ids, int32_t* segs, int32_t* att, uint8_t* fallback) {
   const Tokenizer& t = *reinterpret_cast<Tokenizer*>(h);
   const int L = t.max_len;
-  // a thread per >= 8 texts: spawning one costs ~20 us, a 128-token text ~10 us
+  // a worker per >= 8 texts (a 128-token text is ~10 us of work)
   nthreads = std::max(1, std::min(nthreads, (n + 7) / 8));
   std::vector<int> nfb(nthreads, 0);
   auto work = [&](int tid) {
@@ -197,9 +262,7 @@ int samp_tokenize_batch(samp_tokenizer* h, const char* const* text_a, const char
   if (nthreads == 1) {
     work(0);
   } else {
-    std::vector<std::thread> pool;
-    for (int k = 0; k < nthreads; ++k) pool.emplace_back(work, k);
-    for (auto& th : pool) th.join();
+    reinterpret_cast<Tokenizer*>(h)->pool.run(nthreads, work);
   }
   int total = 0;
   for (int v : nfb) total += v;

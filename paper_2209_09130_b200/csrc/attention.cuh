@@ -41,7 +41,10 @@
 
 namespace samp {
 
-constexpr int ATT_THREADS = 288;   // warp 0: TMA + MMA + TMEM owner; warps 1-8: softmax (2 per row)
+// warp 0: TMA + MMA + TMEM owner; warps 1..4*TPR: softmax, TPR threads per query row
+// (TPR = 2 by default, 4 selectable: see attention.cu).
+template <int TPR> constexpr int att_threads() { return 32 + 128 * TPR; }
+constexpr int ATT_MAX_LEAVES = 8;  // numpy tree leaves for S <= 512
 constexpr int ATT_MAX_KEYS = 512;
 constexpr int ATT_P_CHUNK = 256;   // keys of P written per MMA-2 round
 
@@ -84,13 +87,14 @@ struct AttnLayout {
     v_off = k_off + kv;
     p_off = ((v_off + kv + 1023) / 1024) * 1024;
     x_off = p_off + 128 * pchunk * C::P_ELT;
-    bar_off = x_off + 6 * 128 * 4;
+    bar_off = x_off + (3 * 4 + ATT_MAX_LEAVES + 1) * 128 * 4;   // extremes [3][4][128], leaf sums, denom
     total = bar_off + 64 + 1024;
   }
 };
 
-// named barrier among the 256 softmax threads
-__device__ __forceinline__ void att_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// named barrier among the 128*TPR softmax threads
+template <int TPR>
+__device__ __forceinline__ void att_bar() { asm volatile("bar.sync 1, %0;" :: "n"(128 * TPR) : "memory"); }
 
 constexpr float ATT_EXP_FAST_MIN = NP_EXP2_FAST_MIN;   // x - max >= this: np_exp2_fast is exact
 constexpr float ATT_EXP_LO_CUT = -103.97208404541015625f;
@@ -143,8 +147,8 @@ __device__ __forceinline__ float att_leaf(uint32_t ta, int col, int n, const X2&
   return res;
 }
 
-template <bool F16>
-__global__ void __launch_bounds__(ATT_THREADS, 3)
+template <bool F16, int TPR>
+__global__ void __launch_bounds__(att_threads<TPR>(), TPR == 2 ? 3 : 2)
 attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p, int keys_cap) {
   using C = AttnCfg<F16>;
   extern __shared__ uint8_t smem_raw[];
@@ -179,7 +183,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
   if (threadIdx.x == 0) {
     mbar_init(bar_load, 1);
     mbar_init(bar_s, 1);
-    mbar_init(bar_p, 256);
+    mbar_init(bar_p, 128 * TPR);
     mbar_init(bar_pf, 1);
     fence_barrier_init();
   }
@@ -240,11 +244,12 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
   } else {
     const X2 kx = p.k;
     const int quarter = warp & 3;
-    const int h = int(warp - 1) >> 2;
+    const int h = int(warp - 1) >> 2;                  // 0 .. TPR-1
     const int r = quarter * 32 + lane_id();            // query row within the tile
     const uint32_t ta = tmem + (uint32_t(quarter * 32) << 16);
-    int* ixch = reinterpret_cast<int*>(smem + lay.x_off);     // [3][2][128] pass-1 extremes
-    float* xch = reinterpret_cast<float*>(smem + lay.x_off);  // reused: [2][128] partial sums
+    int* ixch = reinterpret_cast<int*>(smem + lay.x_off);     // [3][4][128] pass-1 extremes
+    float* leafs = reinterpret_cast<float*>(smem + lay.x_off) + 3 * 4 * 128;   // [ATT_MAX_LEAVES][128]
+    float* dsum = leafs + ATT_MAX_LEAVES * 128;                                // [128] row denominators
     // this row's sequence: packed tiles hold whole sequences of S rows (S % 32 == 0, so a
     // warp's 32 rows never straddle two sequences: kbeg is warp-uniform)
     const int sub = cnt > 1 ? min(r / S, cnt - 1) : 0;
@@ -267,7 +272,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     Acc lowest, highest;
     if constexpr (F16) { lowest = -INFINITY; highest = INFINITY; } else { lowest = INT_MIN; highest = INT_MAX; }
     Acc umax = lowest, umin = highest, mmax = lowest;
-    for (int c0 = 32 * h; c0 < nrow; c0 += 64) {
+    for (int c0 = 32 * h; c0 < nrow; c0 += 32 * TPR) {
       uint32_t v[32];
       tmem_ld32(ta + kbeg + c0, v);
       tmem_wait_ld();
@@ -289,13 +294,16 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     }
     {
       Acc* ex = reinterpret_cast<Acc*>(ixch);
-      ex[(0 * 2 + h) * 128 + r] = umax;
-      ex[(1 * 2 + h) * 128 + r] = umin;
-      ex[(2 * 2 + h) * 128 + r] = mmax;
-      att_bar();
-      umax = max(ex[r], ex[128 + r]);
-      umin = min(ex[256 + r], ex[384 + r]);
-      mmax = max(ex[512 + r], ex[640 + r]);
+      ex[(0 * 4 + h) * 128 + r] = umax;
+      ex[(1 * 4 + h) * 128 + r] = umin;
+      ex[(2 * 4 + h) * 128 + r] = mmax;
+      att_bar<TPR>();
+#pragma unroll
+      for (int q = 0; q < TPR; ++q) {
+        umax = max(umax, ex[(0 * 4 + q) * 128 + r]);
+        umin = min(umin, ex[(1 * 4 + q) * 128 + r]);
+        mmax = max(mmax, ex[(2 * 4 + q) * 128 + r]);
+      }
     }
     auto xval = [&](Acc a) -> float {
       if constexpr (F16) return __fmul_rn(a, m); else return __fmul_rn(__int2float_rn(a), m);
@@ -311,7 +319,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     const float2 negmx = f2(-mx, -mx), mm = f2(m, m);
 
     // ---- pass 2: e = exp(x - max) -> TMEM (0 past S)
-    for (int c0 = 32 * h; c0 < nrow; c0 += 64) {
+    for (int c0 = 32 * h; c0 < nrow; c0 += 32 * TPR) {
       uint32_t v[32];
       tmem_ld32(ta + kbeg + c0, v);
       tmem_wait_ld();
@@ -337,23 +345,29 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     }
     tmem_wait_st();
     tc_fence_before();
-    att_bar();                                    // every e of the row is in TMEM
+    att_bar<TPR>();                               // every e of the row is in TMEM
     tc_fence_after();
     if (stamper) stamp[4] = globaltimer();
 
-    // ---- numpy pairwise sum over the row's S values (np.sum = 0 + tree)
-    float part = 0.0f;
+    // ---- numpy pairwise sum over the row's S values (np.sum = 0 + tree): the tree's
+    // leaves (key order, <= 128 keys each) are summed from TMEM by thread h = leaf % TPR,
+    // then thread 0 combines them up the tree
     if (S <= 128) {
-      if (h == 0) part = att_leaf(ta, kbeg, S, kx);
+      if (h == 0) dsum[r] = __fadd_rn(0.0f, att_leaf(ta, kbeg, S, kx));
     } else {                                      // single-sequence tile, kbeg = 0
-      const int n2 = pw_split(S);
-      const int lo = h ? n2 : 0, n = h ? S - n2 : n2;
-      auto leaf = [&](int l, int ln, int) { return att_leaf(ta, lo + l, ln, kx); };
-      part = pw_tree_eval(n, leaf);
+      auto own = [&](int lo, int ln, int li) {
+        if (li % TPR == h) leafs[li * 128 + r] = att_leaf(ta, lo, ln, kx);
+        return 0.0f;
+      };
+      pw_tree_eval(S, own);
+      att_bar<TPR>();
+      if (h == 0) {
+        auto read = [&](int, int, int li) { return leafs[li * 128 + r]; };
+        dsum[r] = __fadd_rn(0.0f, pw_tree_eval(S, read));
+      }
     }
-    xch[h * 128 + r] = part;
-    att_bar();
-    const float denom = S <= 128 ? __fadd_rn(0.0f, xch[r]) : __fadd_rn(0.0f, __fadd_rn(xch[r], xch[128 + r]));
+    att_bar<TPR>();
+    const float denom = dsum[r];
     if (stamper) stamp[5] = globaltimer();
     // denom in [1, S] and e in [0, 1]: the hoisted-reciprocal quotient is exact (numerics.cuh)
     const Recip rden = make_recip(denom), rsm = make_recip(F16 ? 1.0f : p.s_softmax);
@@ -378,7 +392,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     for (int ch = 0; ch < nchunks; ++ch) {
       if (ch > 0) mbar_wait(bar_pf, (ch - 1) & 1);    // previous round consumed the buffer
       const int k_lo = ch * ATT_P_CHUNK, k_hi = min(nkp, k_lo + ATT_P_CHUNK);
-      for (int c0 = k_lo + 32 * h; c0 < k_hi; c0 += 64) {
+      for (int c0 = k_lo + 32 * h; c0 < k_hi; c0 += 32 * TPR) {
         uint32_t w[16] = {};
         const int key0 = c0 - kbeg;                   // sequence-local key of the chunk
         if (key0 >= 0 && key0 < nrow) {               // warp-uniform: the row's own keys
@@ -420,43 +434,46 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     }
 
     if (stamper) stamp[6] = globaltimer();
-    // context rows: h writes output columns [32h, 32h+32)
+    // context rows: h writes output columns [OC*h, OC*h + OC), OC = 64 / TPR
+    constexpr int OC = 64 / TPR;
     mbar_wait(bar_pf, (nchunks - 1) & 1);
     tc_fence_after();
-    uint32_t o[32];
-    tmem_ld32(ta + 32 * h, o);
+    uint32_t o[OC];
+    if constexpr (OC == 32) tmem_ld32(ta + OC * h, o);
+    else tmem_ld16(ta + OC * h, o);
     tmem_wait_ld();
     const Recip rctx = make_recip(F16 ? 1.0f : p.s_ctx);
     float amx_ctx = 0.0f;
     if (live) {
       const size_t orow = size_t(krow0 + q0 + r);
       if constexpr (F16) {
-        __half* dst = static_cast<__half*>(p.ctx_out) + orow * p.hidden + head * 64 + 32 * h;
-        uint32_t w[16];
+        __half* dst = static_cast<__half*>(p.ctx_out) + orow * p.hidden + head * 64 + OC * h;
+        uint32_t w[OC / 2];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
+        for (int j = 0; j < OC; j += 2) {
           __half2 hv = __floats2half2_rn(__uint_as_float(o[j]), __uint_as_float(o[j + 1]));
           w[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
         }
         uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) d4[u] = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+        for (int u = 0; u < OC / 8; ++u) d4[u] = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
         if (p.amax) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) amx_ctx = fmaxf(amx_ctx, fabsf(__uint_as_float(o[j])));
+          for (int j = 0; j < OC; ++j) amx_ctx = fmaxf(amx_ctx, fabsf(__uint_as_float(o[j])));
         }
       } else {
-        int8_t* dst = static_cast<int8_t*>(p.ctx_out) + orow * p.hidden + head * 64 + 32 * h;
-        uint32_t w[8];
+        int8_t* dst = static_cast<int8_t*>(p.ctx_out) + orow * p.hidden + head * 64 + OC * h;
+        uint32_t w[OC / 4];
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < OC; j += 4) {
           float q[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) q[u] = quant_pre_bounded(__fmul_rn(__int2float_rn(int(o[j + u])), p.mult_ctx), rctx);
           w[j / 4] = trunc_pack4_s8(q[0], q[1], q[2], q[3]);
         }
-        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+        for (int u = 0; u < OC / 16; ++u)
+          reinterpret_cast<uint4*>(dst)[u] = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
       }
     }
     if (F16 && p.amax) {

@@ -67,7 +67,9 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in sources]
     if jobs or not os.path.exists(lib):
         cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
-        subprocess.run(cmd, check=True, capture_output=not verbose)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc link failed:\n{r.stderr[-6000:]}")
     return lib
 
 

@@ -1,9 +1,18 @@
+#include "gemm_ln_persistent.cuh"
 #include "kernels.h"
 
 namespace samp {
 
 cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                        const EpiResLN::Params& p, cudaStream_t st) {
+  // persistent clusters only on request (SAMP_LN_PERSISTENT=1): with f32 residuals read
+  // per element it measured slower than one tile per CTA (C5 out-proj 1.92 vs 1.17 ms)
+  if (std::getenv("SAMP_LN_PERSISTENT")) {
+    switch (t.bn_ln * 10 + t.cluster_ln) {
+      case 1924: return launch_gemm_ln_persistent<KIND_F16, 192, 4, 4>(a, b, M, kb, p, st);
+      case 2564: return launch_gemm_ln_persistent<KIND_F16, 256, 3, 4>(a, b, M, kb, p, st);
+    }
+  }
   switch (t.bn_ln * 10 + t.cluster_ln) {
     case 1924: return launch_gemm<KIND_F16, 192, 4, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 2564: return launch_gemm<KIND_F16, 256, 3, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);

@@ -5,19 +5,20 @@ namespace samp {
 
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                        const EpiResLN::Params& p, cudaStream_t st) {
-  // Opt-in (SAMP_LN_PERSISTENT=1): persistent clusters with double-buffered TMEM when there
-  // are more row tiles than co-resident clusters (gemm_ln_persistent.cuh).  Bit-exact, but
-  // measured slower than one tile per CTA (C5 FFN2 1.80 vs 1.57 ms, C4 0.12 vs 0.11 ms:
-  // ncu shows SMs idle ~45% of the kernel), so not the default.
+  // Many more row tiles than co-resident clusters (probed, gemm_ln_persistent.cuh): persistent
+  // clusters with double-buffered TMEM walk the row tiles (C5 FFN2 1.09 vs 1.51 ms at 262k
+  // tokens).  With only a few tiles per cluster the fill/drain and the uneven split lose
+  // (C4 out-proj 72 vs 57 us at 4 tiles/cluster), hence >= 8 tiles per cluster; otherwise
+  // one tile per CTA.  SAMP_NO_LN_PERSISTENT=1 / SAMP_LN_PERSISTENT=1 force either.
   const int mtiles = (M + GEMM_BM - 1) / GEMM_BM;
-  if (std::getenv("SAMP_LN_PERSISTENT") != nullptr) {
+  if (std::getenv("SAMP_NO_LN_PERSISTENT") == nullptr && (mtiles >= 256 || std::getenv("SAMP_LN_PERSISTENT"))) {
     switch (t.bn_ln * 10 + t.cluster_ln) {
       case 1924:
-        if (mtiles > ln_persistent_clusters<KIND_I8, 192, 4, 4>())
+        if (mtiles >= 8 * ln_persistent_clusters<KIND_I8, 192, 4, 4>() || std::getenv("SAMP_LN_PERSISTENT"))
           return launch_gemm_ln_persistent<KIND_I8, 192, 4, 4>(a, b, M, kb, p, st);
         break;
       case 2564:
-        if (mtiles > ln_persistent_clusters<KIND_I8, 256, 3, 4>())
+        if (mtiles >= 8 * ln_persistent_clusters<KIND_I8, 256, 3, 4>() || std::getenv("SAMP_LN_PERSISTENT"))
           return launch_gemm_ln_persistent<KIND_I8, 256, 3, 4>(a, b, M, kb, p, st);
         break;
     }

@@ -23,7 +23,9 @@
 // identical outputs.  Roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps
 // 2..9 epilogue (two threads per row, BN/2 columns each = one numpy subtree).
 #pragma once
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 
 #include "gemm_persistent.cuh"
 
@@ -294,32 +296,61 @@ gemm_ln_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __gri
   }
 }
 
-// clusters that can be co-resident (GPC packing may hold fewer than SMs / CLUSTER)
+// How many clusters of CLUSTER CTAs with `smem` bytes each are really co-resident.  The
+// occupancy API reports 37 clusters of 4 at ~221 KB/CTA on a 148-SM B200, but GPC packing
+// fits 33: a persistent grid of 34+ clusters leaves its last clusters waiting for others
+// to finish and takes ~1.6x longer (measured).  The probe launches every candidate cluster
+// holding its SMs for ~40 us and counts those that started together.
+static __global__ void cluster_probe_kernel(unsigned long long* starts) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    starts[blockIdx.x] = t0;
+    while (globaltimer() - t0 < 40000ull) {
+    }
+  }
+}
+
+static inline int probe_coresident_clusters(int cluster, size_t smem) {
+  const int sms = device_sm_count();
+  const int n = (sms / cluster) * cluster;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, n * sizeof(unsigned long long)) != cudaSuccess) return sms / cluster;
+  cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int together = sms / cluster;
+  if (cudaLaunchKernelEx(&cfg, cluster_probe_kernel, d) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess) {
+    std::vector<unsigned long long> h(n);
+    cudaMemcpy(h.data(), d, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    const unsigned long long t_min = *std::min_element(h.begin(), h.end());
+    int started = 0;
+    for (unsigned long long t : h) started += t < t_min + 20000ull;
+    together = std::max(1, started / cluster);
+  }
+  cudaGetLastError();
+  cudaFree(d);
+  return together;
+}
+
 template <int KIND, int BN, int STAGES, int CLUSTER>
 inline int ln_persistent_clusters() {
   static thread_local int dev = -1, n = 0;
   int d = 0;
   cudaGetDevice(&d);
   if (d != dev) {
-    using Lay = LnPersistLayout<BN, STAGES, CLUSTER>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CLUSTER * 64);
-    cfg.blockDim = dim3(64 + 32 * 8);
-    cfg.dynamicSmemBytes = Lay::TOTAL;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = CLUSTER;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    int c = 0;
-    if (cudaOccupancyMaxActiveClusters(&c, gemm_ln_persistent_kernel<KIND, BN, STAGES, CLUSTER>, &cfg) != cudaSuccess ||
-        c <= 0)
-      c = device_sm_count() / CLUSTER;
-    n = c;
+    n = probe_coresident_clusters(CLUSTER, LnPersistLayout<BN, STAGES, CLUSTER>::TOTAL);
     dev = d;
-    if (std::getenv("SAMP_VERBOSE")) std::fprintf(stderr, "ln_persistent: %d co-resident clusters of %d (BN %d)\n", c, CLUSTER, BN);
+    if (std::getenv("SAMP_VERBOSE")) std::fprintf(stderr, "ln_persistent: %d co-resident clusters of %d (BN %d)\n", n, CLUSTER, BN);
   }
   return n;
 }
@@ -340,7 +371,8 @@ inline cudaError_t launch_gemm_ln_persistent(const CUtensorMap& map_a, const CUt
     configured = dev;
   }
   const int mtiles = (M + GEMM_BM - 1) / GEMM_BM;
-  const int clusters = std::min(mtiles, ln_persistent_clusters<KIND, BN, STAGES, CLUSTER>());
+  int clusters = std::min(mtiles, ln_persistent_clusters<KIND, BN, STAGES, CLUSTER>());
+  if (const char* f = std::getenv("SAMP_LNP_CLUSTERS")) clusters = std::min(mtiles, std::atoi(f));   // measurement
   return launch_ex(kern, dim3(clusters * CLUSTER), dim3(64 + 32 * 8), Lay::TOTAL, stream, CLUSTER, map_a, map_b, M,
                    k_bytes, p);
 }

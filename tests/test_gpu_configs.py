@@ -304,3 +304,21 @@ def test_run_texts_equals_encoded_runs(matcher):
         one = eng.run(enc, plan)
         np.testing.assert_array_equal(res.sequence(i), one.hidden_states)
         np.testing.assert_array_equal(res.logits[i], one.head["logits"][0])
+
+
+@pytest.mark.parametrize("mode,k", [("FP", 0), ("FFN_ONLY", 2), ("MHA_ONLY", 2), ("FULLY_QUANT", 2)])
+def test_persistent_layernorm_all_precisions_identical(mode, k, monkeypatch):
+    """The persistent cluster LN GEMM (forced) gives bit-identical hidden states to the
+    one-tile kernel for every layer kind: int8 and f16 accumulators, int8 / f32 residuals,
+    quantized, dequantized (MHA-only) and f32/f16 outputs."""
+    arch = _archive(768, 12, 3072, "classification", 2, seed=5)
+    rng = np.random.default_rng(3)
+    _calibrate(arch, [(rng.integers(4, 1000, 64).tolist(), [0] * 64) for _ in range(2)])
+    plan = PrecisionPlan.prefix(mode, 2, k)
+    rng = np.random.default_rng(43)
+    encs = [EncodedInput(rng.integers(4, 1000, n).tolist(), [0] * n, n - 5) for n in (128, 96, 200, 64, 128)]
+    base = _engine(arch).run_batch(encs, plan)
+    monkeypatch.setenv("SAMP_LN_PERSISTENT", "1")
+    pers = _engine(arch).run_batch(encs, plan)
+    np.testing.assert_array_equal(pers.hidden_states, base.hidden_states)
+    np.testing.assert_array_equal(pers.logits, base.logits)

@@ -20,7 +20,7 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 SHORT = [("EpiGeluQuantT", "ffn1_i8"), ("EpiQKV", "qkv_i8"), ("EpiGeluQuant", "ffn1_i8"), ("EpiResLN", "ln_i8"), ("EpiF16Out", "f16out"),
-         ("attention_kernel<0>", "attention_i8"), ("attention_kernel<1>", "attention_f16"),
+         ("attention_kernel<0", "attention_i8"), ("attention_kernel<1", "attention_f16"),
          ("embed_kernel", "embed"), ("pooler_kernel", "pooler"), ("classifier_kernel", "classifier")]
 
 

@@ -210,6 +210,15 @@ gemm_ln_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __gri
         if (lane_id() == 0) mbar_arrive(&acc_empty[b]);    // accumulator consumed: next MMA may start
 #pragma unroll
         for (int kk = 0; kk < NC / 32; ++kk) {
+          float rf[32];   // f32 residual (FP layers): 16-byte loads
+          if (!p.res_i8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.res_f32 + rbase + n0 + c0 + 32 * kk) + q)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+              rf[4 * q] = v.x; rf[4 * q + 1] = v.y; rf[4 * q + 2] = v.z; rf[4 * q + 3] = v.w;
+            }
+          }
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
             const int cc = 32 * kk + jj;
@@ -218,7 +227,7 @@ gemm_ln_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __gri
               const uint32_t w = reinterpret_cast<const uint32_t*>(&rv[cc / 16])[(cc % 16) / 4];
               res = deq(int(int8_t((w >> (8 * (cc % 4))) & 0xff)), p.res_scale);
             } else {
-              res = valid ? p.res_f32[rbase + n0 + c0 + cc] : 0.0f;
+              res = rf[jj];
             }
             const uint32_t u = r[cc];
             const float acc = p.acc_is_f32 ? __uint_as_float(u) : __fmul_rn(__int2float_rn(int(u)), p.mult);

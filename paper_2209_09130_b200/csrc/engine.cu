@@ -67,6 +67,7 @@ struct LayerDev {
   double b1_absmax = 0;                 // max|b1|: bounds the FFN1 GELU argument
   CUtensorMap m_qkv_i8, m_wo_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w2_f16;
   CUtensorMap m_wo_i8_64, m_w2_i8_64;    // 64-row boxes: split-K GEMMs for small batches
+  CUtensorMap m_qkv_i8_128;              // 128-row boxes: persistent QKV
   CUtensorMap m_w1_i8[3], m_w1_f16[3];   // FFN1 B operand, box rows FFN1_BN[k]
 };
 
@@ -490,7 +491,12 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     qp.sout0 = f32(sc(e, lsite(i, "attn", "q")));
     qp.sout1 = f32(sc(e, lsite(i, "attn", "k")));
     qp.sout2 = f32(sc(e, lsite(i, "attn", "v")));
-    check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
+    // persistent 128-wide tiles, two CTAs/SM: 35.9k vs 35.8k sentences/s at batch 32 and
+    // batch-1 fully-quant p50 0.525 vs 0.55 ms (twice the CTAs at one row tile)
+    if (!std::getenv("SAMP_QKV_ONETILE") && (3 * H) % 128 == 0)
+      check_launch(e, gemm_qkv_i8(-128, a.a_xq[cur], w.m_qkv_i8_128, T, 3 * H, H, qp, st), "qkv_i8");
+    else
+      check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
     record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
     AttnParams ap{};
     ap.ctx_out = a.ctx_i8;
@@ -804,6 +810,7 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     w.ln2_b = up(t[15], H);
     const Tiles& tl = e->tiles;
     w.m_qkv_i8 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, tl.bn_qkv);
+    w.m_qkv_i8_128 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, 128);
     w.m_wo_i8 = tmap_i8(w.wo_i8, H, H, H, 128, tl.bn_ln);
     w.m_wo_i8_64 = tmap_i8(w.wo_i8, H, H, H, 128, 64);
     for (int k = 0; k < 3; ++k)

@@ -42,8 +42,9 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
 
 cudaError_t gemm_qkv_i8(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                         const EpiQKV::Params& p, cudaStream_t st) {
-  // QKV's epilogue is light (dequant + quantize): two co-resident one-tile CTAs per SM
-  // overlap each other better than one persistent CTA (18.3 vs 18.9 us at 4096 tokens)
+  // bn < 0: persistent kernel with |bn|-wide tiles, two CTAs per SM (engine default, 128);
+  // bn > 0: one tile per CTA (SAMP_QKV_ONETILE=1)
+  if (bn < 0) return by_bn<EpiQKV>(-bn, true, a, b, M, N, kb, p, st);
   return by_bn<EpiQKV>(bn, false, a, b, M, N, kb, p, st);
 }
 

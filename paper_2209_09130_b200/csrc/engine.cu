@@ -1,3 +1,4 @@
+#include <cstdio>
 // The samp_b200 engine: device weights, calibration scales, activation buffers and
 // the per-layer mixed-precision forward (reference Engine, pkg/src/samp/encoder.py:421-530).
 //
@@ -408,6 +409,8 @@ static int tmem_cols_for_keys(int nkp) {
   return c;
 }
 
+static unsigned long long* g_gelu_flags = nullptr;   // SAMP_GELU_FLAGS measurement counter
+
 static uint32_t bits_of(float f) {
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -603,6 +606,10 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     auto ok = e->gelu_fast_ok.find(bits_of(gp.s_out));
     const bool fast = finite && ok != e->gelu_fast_ok.end() && ok->second;
     gp.inv_s = gelu_inv_s(gp.s_out);
+    if (std::getenv("SAMP_GELU_FLAGS")) {   // measurement: count flagged 8-groups per forward
+      if (!g_gelu_flags) cudaMallocManaged(&g_gelu_flags, sizeof(unsigned long long));
+      gp.flag_count = g_gelu_flags;
+    }
     const int k1 = ffn1_bn_index(T, I, e->sms);
     check_launch(e, gemm_gelu_i8(FFN1_BN[k1], fast ? GELU_FAST : finite ? GELU_FINITE : GELU_GENERAL, a.a_ffn_in,
                                  w.m_w1_i8[k1], T, I, H, gp, st), "ffn1_i8");
@@ -1136,6 +1143,12 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       }
     }
     if (io == SAMP_IO_HOST) SAMP_CUDA(cudaStreamSynchronize(st));
+    if (g_gelu_flags && std::getenv("SAMP_GELU_FLAGS")) {
+      SAMP_CUDA(cudaDeviceSynchronize());
+      std::fprintf(stderr, "gelu_fast: %llu flagged 8-groups of %lld\n", *g_gelu_flags,
+                   (long long)T * d.intermediate / 8 * d.num_layers);
+      *g_gelu_flags = 0;
+    }
     if (staged) {
       if (out->logits) std::memcpy(out->logits, e->pinned_out, rows * nl * 4);
       if (out->probs) std::memcpy(out->probs, e->pinned_out + rows * nl, rows * nl * 4);

@@ -382,6 +382,7 @@ struct GeluQuantParams {
   float s_out;
   float inv_s = 0.0f;   // ~1/s_out (GELU_FAST)
   X2 k = x2_consts();   // opaque FFMA2 constants (packed path)
+  unsigned long long* flag_count = nullptr;   // measurement: flagged 8-groups (SAMP_GELU_FLAGS)
 };
 template <int MODE>
 struct EpiGeluQuantT {
@@ -450,6 +451,7 @@ struct EpiGeluQuantT {
             float2 t[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) t[u] = gelu_q_fast2(f2(v[2 * u], v[2 * u + 1]), p.inv_s, k, near);
+            if (near && p.flag_count) atomicAdd(p.flag_count, 1ull);
             if (near) {
               exact8(v, tt, rq, k, w[g / 4], w[g / 4 + 1]);
             } else {

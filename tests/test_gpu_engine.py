@@ -274,3 +274,33 @@ def test_cuda_graph_replay_is_bit_identical(bert2):
     # geometry change invalidates nothing incorrectly
     other = eng.run_batch(encs[:1], plan)
     np.testing.assert_array_equal(other.sequence(0), outs[0].sequence(0))
+
+
+def test_shared_engine_across_threads_is_bitwise_deterministic(bert2):
+    """One Engine shared by several host threads (reference tests/test_encoder.py:340-350:
+    results are bitwise thread-independent): concurrent run / run_batch calls with
+    different plans and geometries equal the same calls made sequentially."""
+    import threading
+    arch, _ = bert2
+    eng = _engine(arch)
+    rng = np.random.default_rng(77)
+    jobs = []
+    for j in range(8):
+        encs = _batch(rng, [(n, n) for n in rng.integers(16, 200, size=1 + j % 3).tolist()])
+        encs = [EncodedInput(e.token_ids, e.segment_ids, len(e.token_ids) - j) for e in encs]
+        mode = ("FULLY_QUANT", "FFN_ONLY", "FP", "MHA_ONLY")[j % 4]
+        jobs.append((encs, PrecisionPlan.prefix(mode, 2, 0 if mode == "FP" else 2)))
+    want = [eng.run_batch(encs, plan).hidden_states for encs, plan in jobs]
+    got = [None] * len(jobs)
+
+    def work(k):
+        for _ in range(3):
+            got[k] = eng.run_batch(*jobs[k]).hidden_states
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for k in range(len(jobs)):
+        np.testing.assert_array_equal(got[k], want[k], err_msg=f"job {k}")

@@ -68,6 +68,7 @@ struct LayerDev {
   double b1_absmax = 0;                 // max|b1|: bounds the FFN1 GELU argument
   CUtensorMap m_qkv_i8, m_wo_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w2_f16;
   CUtensorMap m_wo_i8_64, m_w2_i8_64;    // 64-row boxes: split-K GEMMs for small batches
+  CUtensorMap m_wo_i8_s, m_w2_i8_s, m_wo_f16_s, m_w2_f16_s;   // bn_ln_small-row boxes
   CUtensorMap m_qkv_i8_128;              // 128-row boxes: persistent QKV
   CUtensorMap m_w1_i8[3], m_w1_f16[3];   // FFN1 B operand, box rows FFN1_BN[k]
 };
@@ -113,6 +114,8 @@ static Tiles choose_tiles(int H, int I) {
       t.cluster_ln = c[1];
       break;
     }
+  // one numpy leaf per CTA: H = 8 leaves of 96 (768) or 128 (1024)
+  t.bn_ln_small = (pw_splits_evenly(H, 8) && (H / 8 == 96 || H / 8 == 128)) ? H / 8 : 0;
   return t;
 }
 
@@ -472,7 +475,17 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   const bool next_int8 = i + 1 < L && (prec[i + 1] == SAMP_LAYER_FULL_INT8 || prec[i + 1] == SAMP_LAYER_MHA_INT8);
   Activations& a = e->act;
   LayerDev& w = e->layers[i];
+  // small batches: twice the LN-GEMM CTAs (8-CTA clusters, one numpy leaf each) so each
+  // streams half the weights; SAMP_NO_LN_SMALL=1 keeps the 4-CTA clusters
+  const int mtiles = (T + GEMM_BM - 1) / GEMM_BM;
+  const bool ln_small = e->tiles.bn_ln_small && mtiles * 8 <= e->sms && !std::getenv("SAMP_NO_LN_SMALL");
+  Tiles tsm = e->tiles;
+  if (ln_small) {
+    tsm.bn_ln = tsm.bn_ln_small;
+    tsm.cluster_ln = 8;
+  }
   const Tiles& t = e->tiles;
+  const Tiles& tln = tsm;
   const float eps = f32(e->d.layernorm_eps);
   const int fp16_store = e->d.fp16_storage;
   const bool int8_attn = p == SAMP_LAYER_FULL_INT8 || p == SAMP_LAYER_MHA_INT8;
@@ -535,7 +548,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.out_f16 = a.ln1_f16;
     }
     if (!ln_gemm_splitk(e, "outproj_i8", a.a_ctx_i8, w.m_wo_i8_64, H, lp, st))
-      check_launch(e, gemm_ln_i8(t, a.a_ctx_i8, w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
+      check_launch(e, gemm_ln_i8(tln, a.a_ctx_i8, ln_small ? w.m_wo_i8_s : w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
     record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
   } else {
     record(e, "in_f32", i, a.hid_f32, size_t(T) * H * 4);
@@ -576,7 +589,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.site = cbase + 6;
       lp.site2 = -1;
     }
-    check_launch(e, gemm_ln_f16(t, a.a_ctx_f16, w.m_wo_f16, T, H, 2 * H, lp, st), "outproj_f16");
+    check_launch(e, gemm_ln_f16(tln, a.a_ctx_f16, ln_small ? w.m_wo_f16_s : w.m_wo_f16, T, H, 2 * H, lp, st),
+                 "outproj_f16");
     if (p == SAMP_LAYER_FFN_INT8) record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
     else record(e, "ln1_f32", i, a.ln1_f32, size_t(T) * H * 4);
   }
@@ -618,7 +632,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.res_scale = f32(s_fin);
     lp.mult = mult_of(s_mid, w.s_w[5]);
     if (!ln_gemm_splitk(e, "ffn2_i8", a.a_mid_i8, w.m_w2_i8_64, I, lp, st))
-      check_launch(e, gemm_ln_i8(t, a.a_mid_i8, w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
+      check_launch(e, gemm_ln_i8(tln, a.a_mid_i8, ln_small ? w.m_w2_i8_s : w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
   } else {
     EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
     const int k1 = ffn1_bn_index(T, I, e->sms, false);   // EpiF16Out walks 32-column chunks
@@ -631,7 +645,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.site = 1 + 8 * (i + 1);
       lp.site2 = -1;
     }
-    check_launch(e, gemm_ln_f16(t, a.a_mid_f16, w.m_w2_f16, T, H, 2 * I, lp, st), "ffn2_f16");
+    check_launch(e, gemm_ln_f16(tln, a.a_mid_f16, ln_small ? w.m_w2_f16_s : w.m_w2_f16, T, H, 2 * I, lp, st),
+                 "ffn2_f16");
   }
   if (next_int8) {
     cur ^= 1;
@@ -830,6 +845,12 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     w.m_qkv_f16 = tmap_f16(w.qkv_f16, 3 * H, H, H, 64, tl.bn_qkv);
     w.m_wo_f16 = tmap_f16(w.wo_f16, H, H, H, 64, tl.bn_ln);
     w.m_w2_f16 = tmap_f16(w.w2_f16, H, I, I, 64, tl.bn_ln);
+    if (tl.bn_ln_small) {
+      w.m_wo_i8_s = tmap_i8(w.wo_i8, H, H, H, 128, tl.bn_ln_small);
+      w.m_w2_i8_s = tmap_i8(w.w2_i8, H, I, I, 128, tl.bn_ln_small);
+      w.m_wo_f16_s = tmap_f16(w.wo_f16, H, H, H, 64, tl.bn_ln_small);
+      w.m_w2_f16_s = tmap_f16(w.w2_f16, H, I, I, 64, tl.bn_ln_small);
+    }
     w.loaded = true;
   });
 }

@@ -583,13 +583,14 @@ struct EpiResLNT {
   template <int BN> __host__ __device__ static constexpr int res_ld() { return BN + 16; }
   // cluster exchange (CLUSTER > 1): xpart [2 reductions][4][128] floats + xbar[2] mbarriers
   template <int BN> __host__ __device__ static constexpr int xp_off() { return (RED_FLOATS + 3 * BN) * 4 + 128 * res_ld<BN>(); }
-  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return xp_off<BN>() + 2 * 4 * 128 * 4 + 16; }
+  static constexpr int XP_MAX = 8;   // cluster ranks the exchange buffer holds
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return xp_off<BN>() + 2 * XP_MAX * 128 * 4 + 16; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
   // before the kernel's cluster-wide start barrier: the exchange barriers exist before any
   // peer's st.async can complete on them
   template <int BN>
   __device__ static void cluster_init(uint8_t* smem) {
-    uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * 4 * 128 * 4);
+    uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * XP_MAX * 128 * 4);
     mbar_init(&xb[0], 1);
     mbar_init(&xb[1], 1);
   }
@@ -628,8 +629,8 @@ struct EpiResLNT {
       s = __fadd_rn(hv[c.tile_row], hv[128 + c.tile_row]);
     }
     if constexpr (CLUSTER > 1) {
-      float* xp = reinterpret_cast<float*>(smem + xp_off<BN>()) + red * 4 * 128;
-      uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * 4 * 128 * 4) + red;
+      float* xp = reinterpret_cast<float*>(smem + xp_off<BN>()) + red * XP_MAX * 128;
+      uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * XP_MAX * 128 * 4) + red;
       if (c.ep_tid == 0) mbar_expect_tx(xb, CLUSTER * 128 * 4);
       if (c.half == 0) {
         const uint32_t me = cluster_rank();
@@ -641,8 +642,11 @@ struct EpiResLNT {
       float p[CLUSTER];
 #pragma unroll
       for (int r = 0; r < CLUSTER; ++r) p[r] = xp[r * 128 + c.tile_row];
+      // numpy's tree above equal per-rank subtrees: pairs, then pairs of pairs, ...
       if constexpr (CLUSTER == 2) s = __fadd_rn(p[0], p[1]);
-      else s = __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
+      else if constexpr (CLUSTER == 4) s = __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
+      else s = __fadd_rn(__fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3])),
+                         __fadd_rn(__fadd_rn(p[4], p[5]), __fadd_rn(p[6], p[7])));
     }
     return s;
   }

@@ -13,6 +13,7 @@ namespace samp {
 
 struct Tiles {
   int bn_qkv, bn_ffn1, bn_ln, cluster_ln;
+  int bn_ln_small;   // small batches: LN GEMMs as 8-CTA clusters of H/8 columns (0 = n/a)
 };
 
 // gemm_i8.cu

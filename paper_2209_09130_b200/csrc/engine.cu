@@ -69,7 +69,8 @@ struct LayerDev {
   CUtensorMap m_qkv_i8, m_wo_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w2_f16;
   CUtensorMap m_wo_i8_64, m_w2_i8_64;    // 64-row boxes: split-K GEMMs for small batches
   CUtensorMap m_wo_i8_s, m_w2_i8_s, m_wo_f16_s, m_w2_f16_s;   // bn_ln_small-row boxes
-  CUtensorMap m_qkv_i8_128;              // 128-row boxes: persistent QKV
+  CUtensorMap m_qkv_i8_128, m_qkv_i8_64;   // persistent QKV tile widths
+  CUtensorMap m_qkv_f16_64;                // small-batch f16 QKV
   CUtensorMap m_w1_i8[3], m_w1_f16[3];   // FFN1 B operand, box rows FFN1_BN[k]
 };
 
@@ -486,6 +487,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   }
   const Tiles& t = e->tiles;
   const Tiles& tln = tsm;
+  // QKV tiles 64 wide when 128-wide ones would leave most SMs idle (batch 1: 36 CTAs, not 18)
+  const bool qkv_narrow = mtiles * (3 * H / 128) * 2 <= e->sms && (3 * H) % 64 == 0 && !std::getenv("SAMP_NO_QKV_NARROW");
   const float eps = f32(e->d.layernorm_eps);
   const int fp16_store = e->d.fp16_storage;
   const bool int8_attn = p == SAMP_LAYER_FULL_INT8 || p == SAMP_LAYER_MHA_INT8;
@@ -510,7 +513,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     // persistent 128-wide tiles, two CTAs/SM: 35.9k vs 35.8k sentences/s at batch 32 and
     // batch-1 fully-quant p50 0.525 vs 0.55 ms (twice the CTAs at one row tile)
     if (!std::getenv("SAMP_QKV_ONETILE") && (3 * H) % 128 == 0)
-      check_launch(e, gemm_qkv_i8(-128, a.a_xq[cur], w.m_qkv_i8_128, T, 3 * H, H, qp, st), "qkv_i8");
+      check_launch(e, qkv_narrow ? gemm_qkv_i8(-64, a.a_xq[cur], w.m_qkv_i8_64, T, 3 * H, H, qp, st)
+                                 : gemm_qkv_i8(-128, a.a_xq[cur], w.m_qkv_i8_128, T, 3 * H, H, qp, st), "qkv_i8");
     else
       check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
     record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
@@ -555,7 +559,10 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     float* cal = e->calib_amax;
     const int cbase = 1 + 8 * i;   // activation_sites order: attn.in q k v softmax out_in ffn.in ffn.mid
     EpiF16Out::Params qp{a.qkv_f16, 3 * H, w.qkv_b, 0, cal, cbase + 1, H};
-    check_launch(e, gemm_f16out(t.bn_qkv, a.a_hid_f16, w.m_qkv_f16, T, 3 * H, 2 * H, qp, st), "qkv_f16");
+    if (qkv_narrow)   // small batches: 64-wide tiles, 4x the CTAs of the 256-wide default
+      check_launch(e, gemm_f16out(64, a.a_hid_f16, w.m_qkv_f16_64, T, 3 * H, 2 * H, qp, st), "qkv_f16");
+    else
+      check_launch(e, gemm_f16out(t.bn_qkv, a.a_hid_f16, w.m_qkv_f16, T, 3 * H, 2 * H, qp, st), "qkv_f16");
     AttnParams ap{};
     ap.ctx_out = a.ctx_f16;
     ap.tile_seq = e->geo.d_tile_seq;
@@ -833,6 +840,7 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     const Tiles& tl = e->tiles;
     w.m_qkv_i8 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, tl.bn_qkv);
     w.m_qkv_i8_128 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, 128);
+    w.m_qkv_i8_64 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, 64);
     w.m_wo_i8 = tmap_i8(w.wo_i8, H, H, H, 128, tl.bn_ln);
     w.m_wo_i8_64 = tmap_i8(w.wo_i8, H, H, H, 128, 64);
     for (int k = 0; k < 3; ++k)
@@ -843,6 +851,7 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     w.m_w2_i8 = tmap_i8(w.w2_i8, H, I, I, 128, tl.bn_ln);
     w.m_w2_i8_64 = tmap_i8(w.w2_i8, H, I, I, 128, 64);
     w.m_qkv_f16 = tmap_f16(w.qkv_f16, 3 * H, H, H, 64, tl.bn_qkv);
+    w.m_qkv_f16_64 = tmap_f16(w.qkv_f16, 3 * H, H, H, 64, 64);
     w.m_wo_f16 = tmap_f16(w.wo_f16, H, H, H, 64, tl.bn_ln);
     w.m_w2_f16 = tmap_f16(w.w2_f16, H, I, I, 64, tl.bn_ln);
     if (tl.bn_ln_small) {

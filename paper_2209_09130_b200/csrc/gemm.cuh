@@ -451,7 +451,9 @@ struct EpiGeluQuantT {
             float2 t[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) t[u] = gelu_q_fast2(f2(v[2 * u], v[2 * u + 1]), p.inv_s, k, near);
+#ifdef SAMP_GELU_FLAG_COUNT   // measurement build only (costs ~1 us per FFN1 launch)
             if (near && p.flag_count) atomicAdd(p.flag_count, 1ull);
+#endif
             if (near) {
               exact8(v, tt, rq, k, w[g / 4], w[g / 4 + 1]);
             } else {

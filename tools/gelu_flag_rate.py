@@ -1,3 +1,7 @@
+"""GELU fast-path fallback rate on the bench batch.  Needs a measurement build:
+    python tools/build_variant.py flags SAMP_GELU_FLAG_COUNT=1
+    SAMP_B200_LIB=abtest/flags/libsamp_b200.so python tools/gelu_flag_rate.py
+"""
 import ctypes, os, sys
 sys.path.insert(0, os.getcwd())
 os.environ["SAMP_GELU_FLAGS"] = "1"

@@ -379,8 +379,9 @@ def run_samp(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic (random ids, random-init weights seed 0; reference-calibrated scales)",
-            "config": {"workload": wl.desc, "model": wl.model, "plan": f"{wl.mode} k={L}", "batch_per_gpu": BATCH,
-                       "seq_len": SEQ, "global_batch": BATCH * world, "parallelism": f"replicas x{world} (batch-sharded)",
+            "config": {"workload": wl.desc, "encoder": wl.model, "plan": f"{wl.mode} k={L}",
+                       "sequences_per_gpu": BATCH, "tokens_per_sequence": SEQ, "sequences_total": BATCH * world,
+                       "sharding": f"independent replicas x{world} (sequences partitioned, no collective)",
                        "l2": "flushed before every timed step (256 MiB write)",
                        "calibration": "reference (tests/golden)" if wl.key == "c2" else "on-device, 8 rng(1) sequences"},
             "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
@@ -476,7 +477,7 @@ def run_reference(args):
         "ms_per_step": round(t_all * 1e3 / args.steps, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int8", "data": "synthetic",
         "config": {"workload": "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 (configs[1])",
-                   "model": MODEL, "plan": "FULLY_QUANT k=12", "step_sample": f"{n} sentences of the batch"},
+                   "encoder": MODEL, "plan": "FULLY_QUANT k=12", "step_sample": f"{n} sentences of the batch"},
         "cpu_baseline": {"value": round(value, 4), "unit": "sentences/s", "cores": cores,
                          "kind": "port", "sample": f"{n} x 128-token sentences per step"},
         "e2e": {"value": round(value, 4), "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

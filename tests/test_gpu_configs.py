@@ -322,3 +322,21 @@ def test_persistent_layernorm_all_precisions_identical(mode, k, monkeypatch):
     pers = _engine(arch).run_batch(encs, plan)
     np.testing.assert_array_equal(pers.hidden_states, base.hidden_states)
     np.testing.assert_array_equal(pers.logits, base.logits)
+
+
+def test_tiny_and_odd_sequence_lengths_bit_exact():
+    """Sequences of 1..17 tokens (numpy pairwise leaves with n < 8, tails of 1..7, one-key
+    softmax rows, single-row tiles) and att_len 0 / 1 / S, mixed in one packed batch."""
+    arch = _archive(768, 12, 3072, "classification", 2, seed=5)
+    rng = np.random.default_rng(3)
+    model = _calibrate(arch, [(rng.integers(4, 1000, 64).tolist(), [0] * 64) for _ in range(2)])
+    eng = _engine(arch)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix("FULLY_QUANT", L, L)
+    rng = np.random.default_rng(51)
+    specs = [(1, 1), (2, 2), (7, 7), (8, 8), (9, 9), (15, 15), (16, 16), (17, 17), (2, 1), (9, 0), (13, 6), (1, 0)]
+    encs = [EncodedInput(rng.integers(4, 1000, S).tolist(), [0] * S, att) for S, att in specs]
+    batch = eng.run_batch(encs, plan)
+    for s, enc in enumerate(encs):
+        want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
+        np.testing.assert_array_equal(batch.sequence(s), want, err_msg=f"spec {specs[s]}")

@@ -319,12 +319,22 @@ def run_samp(args):
     ops = gemm_ops(T, H, I)
     ops["attention_i8"] = 4 * BATCH * SEQ * SEQ * H
     ops["attention_f16"] = 4 * BATCH * SEQ * SEQ * H
+    # HBM-bound kernels: algorithmic bytes per launch (DESIGN.md kernel table): the embed
+    # reads each token's F32 word row and writes its row (int8 on INT8 plans), plus ids /
+    # segments / positions; position / type rows and gamma / beta are read once
+    out_bytes = 1 if wl.mode == "FULLY_QUANT" else 6     # int8, or f32 + f16 rows
+    hbm_bytes = {"embed": T * (4 * H + out_bytes * H + 12) + SEQ * 4 * H + 2 * 4 * H + 2 * 4 * H}
+    hbm_peak = (json.load(open(PEAKS)).get("hbm_gbs") if os.path.exists(PEAKS) else None) or 6650.0
     kernels = {}
     for name, (tot_ms, n) in prof.items():
         avg = tot_ms / n
         rec = {"avg_us": round(avg * 1e3, 2), "launches": n, "share": None}
         if name in ops:
             rec["achieved_tops"] = round(ops[name] / (avg * 1e-3) / 1e12, 1)
+        if name in hbm_bytes:
+            gbs = hbm_bytes[name] / (avg * 1e-3) / 1e9
+            rec["achieved_gbs"] = round(gbs, 1)
+            rec["hbm_frac"] = round(gbs / hbm_peak, 4)
         kernels[name] = rec
     total = sum(v[0] for v in prof.values())
     for name, (tot_ms, _) in prof.items():

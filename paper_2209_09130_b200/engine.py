@@ -136,6 +136,17 @@ class Engine:
 
     def check_plan(self, plan: PrecisionPlan) -> CalibrationTable | None:
         """reference encoder.py:456-470 (same messages)."""
+        table = self.calibration
+        # a plan already checked against this very table, unchanged since: nothing to redo
+        key = (plan.layer_precisions, table.version if table is not None else -1,
+               len(table.entries) if table is not None else -1)
+        if key == getattr(self, "_checked_key", None) and table is getattr(self, "_checked_table", None):
+            return table
+        self._check_plan_uncached(plan)
+        self._checked_key, self._checked_table = key, table
+        return table
+
+    def _check_plan_uncached(self, plan: PrecisionPlan) -> CalibrationTable | None:
         if plan.num_layers != self.manifest.num_layers:
             raise ConfigurationError(f"plan covers {plan.num_layers} layers, model has {self.manifest.num_layers}")
         need = plan.required_sites()

@@ -432,7 +432,106 @@ def _blas_threads():
         return os.cpu_count() or 1
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_package():
+    """The reference's own `samp` package, installed unmodified into baseline/_ref
+    (pip install --target; it travels to the GPU box with the snapshot).  Its snapshot
+    lacks samp/tokenization.py, which five of its modules import, so a staged copy gets our
+    restatement (paper_2209_09130_b200/tokenization.py, pinned to the reference's goldens)
+    dropped in; every other file is the reference's.  None when not installed."""
+    import shutil
+    import tempfile
+    src = os.path.join(REF_DIR, "samp")
+    if not os.path.isdir(src):
+        return None
+    stage = tempfile.mkdtemp(prefix="samp_ref_")
+    shutil.copytree(src, os.path.join(stage, "samp"))
+    if not os.path.exists(os.path.join(stage, "samp", "tokenization.py")):
+        shutil.copy(os.path.join(ROOT, "paper_2209_09130_b200", "tokenization.py"),
+                    os.path.join(stage, "samp", "tokenization.py"))
+    sys.path.insert(0, stage)
+    try:
+        import samp  # noqa: F401
+        import samp.encoder
+        import samp.tasks
+        import samp.synthetic
+        import samp.quantization
+        return samp
+    except Exception:
+        return None
+    finally:
+        sys.path.remove(stage)
+
+
+_REF_RUNNERS = {}
+
+
+def reference_runner(wl):
+    """A callable timing the reference's own Engine.run + tasks.classify/tag (numpy, its own
+    code) on n sentences of the bench workload: the bench weights rebuilt by its
+    synthetic.build_archive (same recipe and seed, fingerprint-checked against ours) and the
+    bench calibration.  Built once per workload; None when the package is not installed."""
+    if wl.key in _REF_RUNNERS:
+        return _REF_RUNNERS[wl.key]
+    runner = None
+    samp = _reference_package()
+    if samp is not None:
+        from paper_2209_09130_b200.synthetic import BERT_SHAPES
+        shapes = BERT_SHAPES[wl.model]
+        base = len(samp.tokenization.SPECIAL_TOKENS) + len(samp.synthetic.DEFAULT_WORDS)
+        vocab = samp.synthetic.tiny_vocab(512, [f"[unused{i}]" for i in range(30522 - base)])
+        arch = samp.synthetic.build_archive(task=wl.task, num_labels=wl.labels, max_position=512, seed=0,
+                                            weight_scale=0.02, vocab=vocab, **shapes)
+        ours = build_model(wl)
+        if arch.fingerprint == ours.fingerprint and ours.calibration is not None:
+            ref_table = samp.quantization.CalibrationTable(model_fingerprint=arch.fingerprint)
+            for site, e in ours.calibration.entries.items():
+                ref_table.observe(site, np.array([e.amax], np.float32))
+            arch.calibration = ref_table
+            eng = samp.encoder.Engine(arch)
+            plan = samp.encoder.PrecisionPlan.prefix(wl.mode, shapes["num_layers"], shapes["num_layers"])
+            warm = [False]
+
+            def runner(n_sent):
+                seq_start, att, ids, segs = synthetic_batch(0, n_sent, wl.seq, wl.pairs)
+                encs = [samp.tokenization.EncodedInput(ids[seq_start[s]:seq_start[s + 1]].tolist(),
+                                                       segs[seq_start[s]:seq_start[s + 1]].tolist(), int(att[s]))
+                        for s in range(n_sent)]
+                if not warm[0]:
+                    eng.run(encs[0], plan)        # the reference's lazy INT8 weight cache
+                    warm[0] = True
+                t0 = time.perf_counter()
+                for s, enc in enumerate(encs):
+                    out = eng.run(enc, plan)
+                    if wl.task == "sequence_labeling":
+                        samp.tasks.tag(arch, out, int(att[s]))
+                    else:
+                        samp.tasks.classify(arch, out)
+                return n_sent / (time.perf_counter() - t0)
+    _REF_RUNNERS[wl.key] = runner
+    return runner
+
+
 def cpu_baseline(arch, plan, args, n_sent=None, wl=None):
+    """The reference's CPU path on a bounded sample of the same workload: the reference's
+    own package when installed in baseline/_ref (kind "reference"), else the oracle port."""
+    wl = wl or WORKLOADS["c2"]
+    n = n_sent or (args.cpu_sentences if wl.key == "c2" else 2)
+    runner = reference_runner(wl) if wl.key == "c2" else None
+    if runner is not None:
+        v = runner(n)
+        if v is not None:
+            return {"value": round(v, 4), "unit": "sentences/s", "cores": _blas_threads(), "kind": "reference",
+                    "sample": f"{n} of the {wl.batch} x {wl.seq}-token sentences, {wl.mode} "
+                              f"{arch.manifest.num_layers}/{arch.manifest.num_layers} + {wl.task} head, the "
+                              f"reference's own samp.encoder.Engine.run + samp.tasks (numpy, OpenBLAS threads), "
+                              f"installed in baseline/_ref"}
+    return cpu_baseline_port(arch, plan, args, n_sent, wl)
+
+
+def cpu_baseline_port(arch, plan, args, n_sent=None, wl=None):
     """The reference's CPU path (oracle port) on a bounded sample of the same workload."""
     from oracle import samp_oracle as orc
 
@@ -474,11 +573,12 @@ def run_reference(args):
     with _all_host_threads():
         for _ in range(args.warmup):
             cpu_baseline(arch, plan, args, n_sent=1)
+        kind = "port"
         for _ in range(args.steps):
-            t0 = time.perf_counter()
             r = cpu_baseline(arch, plan, args, n_sent=n)
-            t_all += time.perf_counter() - t0
+            t_all += n / r["value"]          # the timed sentences only (no per-step set-up)
             vals.append(r["value"])
+            kind = r["kind"]
         cores = _blas_threads()
     value = n * args.steps / t_all
     line = {
@@ -489,7 +589,9 @@ def run_reference(args):
         "config": {"workload": "BERT-base fully-quantized INT8 12/12, batch 32 x seq 128 (configs[1])",
                    "encoder": MODEL, "plan": "FULLY_QUANT k=12", "step_sample": f"{n} sentences of the batch"},
         "cpu_baseline": {"value": round(value, 4), "unit": "sentences/s", "cores": cores,
-                         "kind": "port", "sample": f"{n} x 128-token sentences per step"},
+                         "kind": kind, "sample": f"{n} x 128-token sentences per step" + (
+                             ", the reference's own samp package (baseline/_ref)" if kind == "reference"
+                             else ", oracle port of the reference")},
         "e2e": {"value": round(value, 4), "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

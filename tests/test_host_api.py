@@ -192,3 +192,18 @@ def test_selectors_and_ranking():
         al.Profile(FULLY_QUANT, [al.ProfilePoint(2, 1, 1, 1), al.ProfilePoint(1, 1, 1, 1)])
     with pytest.raises(ConfigurationError):
         al.allocate_decay_aware(prof, "throughput")
+
+
+def test_encoder_module_mirrors_reference_names():
+    """`samp.encoder` users find the reference module's public names (encoder.py:45-87,
+    :139-142, :421) in paper_2209_09130_b200.encoder."""
+    from paper_2209_09130_b200 import encoder as enc
+    for name in ("FP", "FULLY_QUANT", "FFN_ONLY", "LAYER_FP", "LAYER_FFN_INT8", "LAYER_FULL_INT8", "EMBED_OUT_SITE",
+                 "ATTENTION_MASK_VALUE", "attn_in_site", "attn_site", "ffn_site", "activation_sites",
+                 "PrecisionPlan"):
+        assert hasattr(enc, name), name
+    assert (enc.FP, enc.FULLY_QUANT, enc.FFN_ONLY) == ("FP", "FULLY_QUANT", "FFN_ONLY")
+    assert (enc.LAYER_FFN_INT8, enc.LAYER_FULL_INT8, enc.EMBED_OUT_SITE) == ("FFN_ONLY_INT8", "FULL_INT8", "embed.out")
+    sites = enc.activation_sites(2)
+    assert sites[0] == "embed.out" and len(sites) == 1 + 8 * 2
+    assert enc.ATTENTION_MASK_VALUE == np.float32(-10000.0)

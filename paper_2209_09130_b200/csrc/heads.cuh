@@ -81,7 +81,6 @@ __device__ __forceinline__ void softmax_argmax(const float* lg, float* pr, int* 
 static __global__ void __launch_bounds__(HEAD_THREADS) pooler_kernel(const HeadParams p) {
   extern __shared__ float sh[];           // hs [KQ][32] then partials [8][32 seqs][32 cols]
   pdl_trigger();
-  pdl_wait();
   const int H = p.hidden_size, KQ = H / POOL_KSPLIT, kw = KQ / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * POOL_COLS + lane;
@@ -94,6 +93,7 @@ static __global__ void __launch_bounds__(HEAD_THREADS) pooler_kernel(const HeadP
 #pragma unroll
   for (int i = 0; i < POOL_MAX_KW; ++i)
     wv[i] = i < kw ? __ldg(p.pool_w + size_t(k_base + warp * kw + i) * H + j) : 0.0f;
+  pdl_wait();   // weights above are constant: fetched while the last encoder kernel drains
   for (int idx = threadIdx.x; idx < POOL_SEQS * KQ; idx += HEAD_THREADS) {
     const int s = idx / KQ, k = idx - s * KQ;
     hs[k * POOL_SEQS + s] = s < ns ? p.hidden[size_t(p.seq_start[s0 + s]) * H + k_base + k] : 0.0f;

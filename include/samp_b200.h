@@ -108,6 +108,16 @@ int samp_forward(samp_engine* e, const uint8_t* layer_prec, int32_t nseq, const 
 int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_start, const int32_t* att_len,
                    const int32_t* ids, const int32_t* segs, double* amax_out);
 
+/* analyze-quant code usage (replaces the tap + quantize + code_usage loop of
+ * cli.py:284-292 / quantization.py:190-193): one forward of the packed batch (host arrays)
+ * under layer_prec with histogram taps on the INT8 codes the kernels write;
+ * counts[(1 + 8L) * 256] (activation_sites order, index code + 128) are overwritten.
+ * Sites the plan keeps in floating point read zero.  Codes are bit-exact with the
+ * reference's, so the histograms equal its per-site code_usage sums. */
+int samp_code_usage(samp_engine* e, const uint8_t* layer_prec, int32_t nseq, const int32_t* seq_start,
+                    const int32_t* att_len, const int32_t* ids, const int32_t* segs,
+                    unsigned long long* counts);
+
 /* CUDA-graph replay of the forward per (plan, batch geometry, head): on by default;
  * a key is captured on its second use and replayed afterwards */
 int samp_set_graphs(samp_engine* e, int on);

@@ -60,6 +60,8 @@ SIGNATURES = [
                                     ctypes.POINTER(Outputs), ctypes.c_void_p]),
     ("samp_calibrate", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    ("samp_code_usage", ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int32, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("samp_set_graphs", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("samp_sync", ctypes.c_int, [ctypes.c_void_p]),
     ("samp_set_capture", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

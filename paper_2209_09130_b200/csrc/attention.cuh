@@ -65,6 +65,7 @@ struct AttnParams {
   int site_sm, site_ctx;      // L.attn.softmax / L.attn.out_in
   X2 k = x2_consts();         // opaque FFMA2 constants (numerics.cuh)
   unsigned long long* stamps = nullptr;   // measurement only: 8 %globaltimer stamps per CTA
+  unsigned long long* hist = nullptr;     // INT8 code-usage tap: [256] counts of the P codes
 };
 
 template <bool F16>
@@ -77,7 +78,7 @@ struct AttnCfg {
 
 template <bool F16>
 struct AttnLayout {
-  int q_off, k_off, v_off, p_off, x_off, bar_off, total;
+  int q_off, k_off, v_off, p_off, x_off, bar_off, hist_off, total;
   __host__ __device__ AttnLayout(int keys_cap) {
     using C = AttnCfg<F16>;
     const int kv = ((keys_cap + 63) / 64) * 64 * C::ROW_BYTES;
@@ -88,7 +89,8 @@ struct AttnLayout {
     p_off = ((v_off + kv + 1023) / 1024) * 1024;
     x_off = p_off + 128 * pchunk * C::P_ELT;
     bar_off = x_off + (3 * 4 + ATT_MAX_LEAVES + 1) * 128 * 4;   // extremes [3][4][128], leaf sums, denom
-    total = bar_off + 64 + 1024;
+    hist_off = bar_off + 64;                                    // [256] u32 code-usage bins
+    total = hist_off + 1024 + 1024;
   }
 };
 
@@ -188,6 +190,9 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, p.tmem_cols);
+  unsigned int* hist_s = p.hist ? reinterpret_cast<unsigned int*>(smem + lay.hist_off) : nullptr;
+  if (hist_s)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist_s[i] = 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -383,6 +388,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
             make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
     };
     float amx_sm = 0.0f;
+    unsigned int zeros = 0;   // code-usage tap: zero codes counted in registers
     const float2 rden_r = f2(rden.r, rden.r), rden_ns = f2(-rden.s, -rden.s);
     const float2 rsm_r = f2(rsm.r, rsm.r), rsm_ns = f2(-rsm.s, -rsm.s);
     auto div_pair = [&](float2 x, float2 rr, float2 ns) {       // div_fast on a pair
@@ -423,6 +429,15 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
                 q[u].y = key0 + j + 2 * u + 1 < S ? q[u].y : 0.0f;
               }
               w[j / 4] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
+              if (hist_s && live) {   // code-usage tap over the row's S keys (masked ones included)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                  const int c = int(int8_t(w[j / 4] >> (8 * b)));
+                  if (key0 + j + b >= S) continue;
+                  if (c == 0) ++zeros;
+                  else atomicAdd(&hist_s[c + 128], 1u);
+                }
+              }
             }
           }
         }
@@ -432,6 +447,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
       tc_fence_before();
       mbar_arrive(bar_p);
     }
+    if (hist_s && zeros) atomicAdd(&hist_s[128], zeros);
 
     if (stamper) stamp[6] = globaltimer();
     // context rows: h writes output columns [OC*h, OC*h + OC), OC = 64 / TPR
@@ -487,6 +503,9 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     tc_fence_after();
     tmem_dealloc(tmem, p.tmem_cols);
   }
+  if (hist_s)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      if (hist_s[i]) atomicAdd(&p.hist[i], (unsigned long long)hist_s[i]);
   if (stamp && threadIdx.x == 0) stamp[7] = globaltimer();
 }
 

@@ -172,6 +172,7 @@ struct samp_engine {
   int stamp_cap = 0;
   std::vector<std::pair<std::string, int>> stamp_launches;   // (name, CTAs) per GEMM launch
   float* calib_amax = nullptr;    // non-null while samp_calibrate runs: per-site amax taps
+  unsigned long long* usage = nullptr;   // non-null while samp_code_usage runs: [1+8L][256] bins
   struct GraphEntry {
     cudaGraphExec_t exec;
     int launches;
@@ -399,6 +400,13 @@ static void run_kernel(samp_engine* e, const char* what, F&& fn) {
 }
 #define check_launch(E, CALL, NAME) run_kernel((E), (NAME), [&]() { return (CALL); })
 
+// code-usage tap (analyze-quant): histogram of the int8 codes a stage just wrote at an
+// activation site (activation_sites order), when samp_code_usage is running
+static void usage_tap(samp_engine* e, int site, const int8_t* src, int rows, int cols, int ld) {
+  if (!e->usage) return;
+  check_launch(e, launch_code_hist(src, rows, cols, ld, e->usage + size_t(site) * 256, e->stream_in_use), "code_hist");
+}
+
 static void launch_attention(samp_engine* e, bool f16, const AttnParams& p) {
   const Geometry& g = e->geo;
   auto stamped = [&]() { AttnParams q = p; q.stamps = g_gemm_stamps; return q; };
@@ -499,6 +507,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   if (int8_attn) {
     s_in = sc(e, input_site(i));
     record(e, "in_q", i, a.xq[cur], size_t(T) * H);
+    usage_tap(e, i == 0 ? 0 : 1 + 8 * i, a.xq[cur], T, H, H);
     EpiQKV::Params qp{};
     qp.out = a.qkv_i8;
     qp.ldo = 3 * H;
@@ -518,6 +527,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     else
       check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
     record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
+    for (int k = 0; k < 3; ++k) usage_tap(e, 1 + 8 * i + 1 + k, a.qkv_i8 + k * H, T, H, 3 * H);
     AttnParams ap{};
     ap.ctx_out = a.ctx_i8;
     ap.tile_seq = e->geo.d_tile_seq;
@@ -533,8 +543,10 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.mult_ctx = mult_of(ssm, sv);
     ap.s_ctx = f32(sc(e, lsite(i, "attn", "out_in")));
     ap.tmem_cols = tmem_cols_for_keys(e->geo.max_nkp);
+    if (e->usage) ap.hist = e->usage + size_t(1 + 8 * i + 4) * 256;
     launch_attention(e, false, ap);
     record(e, "ctx_q", i, a.ctx_i8, size_t(T) * H);
+    usage_tap(e, 1 + 8 * i + 5, a.ctx_i8, T, H, H);
     EpiResLN::Params lp{};
     lp.bias = w.ob;
     lp.res_i8 = a.xq[cur];
@@ -554,6 +566,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     if (!ln_gemm_splitk(e, "outproj_i8", a.a_ctx_i8, w.m_wo_i8_64, H, lp, st))
       check_launch(e, gemm_ln_i8(tln, a.a_ctx_i8, ln_small ? w.m_wo_i8_s : w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
     record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
+    usage_tap(e, 1 + 8 * i + 6, a.ffn_in_i8, T, H, H);
   } else {
     record(e, "in_f32", i, a.hid_f32, size_t(T) * H * 4);
     float* cal = e->calib_amax;
@@ -598,8 +611,12 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     }
     check_launch(e, gemm_ln_f16(tln, a.a_ctx_f16, ln_small ? w.m_wo_f16_s : w.m_wo_f16, T, H, 2 * H, lp, st),
                  "outproj_f16");
-    if (p == SAMP_LAYER_FFN_INT8) record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
-    else record(e, "ln1_f32", i, a.ln1_f32, size_t(T) * H * 4);
+    if (p == SAMP_LAYER_FFN_INT8) {
+      record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
+      usage_tap(e, 1 + 8 * i + 6, a.ffn_in_i8, T, H, H);
+    } else {
+      record(e, "ln1_f32", i, a.ln1_f32, size_t(T) * H * 4);
+    }
   }
 
   // ---------------- feed-forward block; output goes to xq[cur^1] (codes) or hid_f32/f16
@@ -635,6 +652,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     check_launch(e, gemm_gelu_i8(FFN1_BN[k1], fast ? GELU_FAST : finite ? GELU_FINITE : GELU_GENERAL, a.a_ffn_in,
                                  w.m_w1_i8[k1], T, I, H, gp, st), "ffn1_i8");
     record(e, "mid_q", i, a.mid_i8, size_t(T) * I);
+    usage_tap(e, 1 + 8 * i + 7, a.mid_i8, T, I, I);
     lp.res_i8 = a.ffn_in_i8;
     lp.res_scale = f32(s_fin);
     lp.mult = mult_of(s_mid, w.s_w[5]);
@@ -973,6 +991,34 @@ extern "C" int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_s
   return rc;
 }
 
+// analyze-quant (reference cli.py:269-292): one forward under `prec` with the code-usage
+// taps on; counts[(site) * 256 + code + 128] += occurrences of each INT8 code the kernels
+// wrote at every activation site the plan quantizes (activation_sites order, 1 + 8L sites;
+// sites the plan keeps in floating point stay zero).
+extern "C" int samp_code_usage(samp_engine* e, const uint8_t* prec, int32_t nseq, const int32_t* seq_start,
+                               const int32_t* att_len, const int32_t* ids, const int32_t* segs,
+                               unsigned long long* counts) {
+  int rc = SAMP_OK;
+  rc = guarded([&] {
+    const size_t n = size_t(1 + 8 * e->d.num_layers) * 256;
+    SAMP_CUDA(cudaSetDevice(e->device));
+    unsigned long long* dev = e->mem.alloc<unsigned long long>(n);
+    SAMP_CUDA(cudaMemset(dev, 0, n * sizeof(unsigned long long)));
+    e->usage = dev;
+    samp_outputs none{};
+    const int r = samp_forward(e, prec, nseq, seq_start, att_len, ids, segs, SAMP_IO_HOST, &none, nullptr);
+    e->usage = nullptr;
+    if (r != SAMP_OK) {
+      e->mem.release(dev);
+      throw SampError(r, samp_last_error());
+    }
+    SAMP_CUDA(cudaMemcpy(counts, dev, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    e->mem.release(dev);
+  });
+  e->usage = nullptr;
+  return rc;
+}
+
 extern "C" int samp_sync(samp_engine* e) {
   return guarded([&] { SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use)); });
 }
@@ -1121,7 +1167,7 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
     // ---------------- device work: replay a captured CUDA graph for this (plan, batch
     // geometry, head) when one exists; capture on the second sighting of a key (the first
     // run also configures every kernel's smem attributes outside of capture)
-    const bool graphable = e->graphs_enabled && !e->capture && !e->profiling && !e->calib_amax;
+    const bool graphable = e->graphs_enabled && !e->capture && !e->profiling && !e->calib_amax && !e->usage;
     std::string key;
     if (graphable) {
       key.assign(reinterpret_cast<const char*>(prec), L);

@@ -49,5 +49,8 @@ cudaError_t launch_tag(const HeadParams& p, cudaStream_t st);
 cudaError_t launch_pack_weight(const float* w, int K, int N, float scale, int8_t* out_i8, __half* out_f16,
                                int row_off, cudaStream_t st);
 cudaError_t launch_transpose_f32(const float* w, int K, int N, float* out, cudaStream_t st);
+// code-usage tap: bins[256] += histogram of an int8 [rows][cols] matrix (row stride ld)
+cudaError_t launch_code_hist(const int8_t* src, int rows, int cols, int ld, unsigned long long* bins,
+                             cudaStream_t st);
 
 }  // namespace samp

@@ -111,4 +111,45 @@ cudaError_t launch_transpose_f32(const float* w, int K, int N, float* out, cudaS
   return cudaGetLastError();
 }
 
+// code-usage tap: bins[c + 128] += #{codes == c} over rows x cols of an int8 matrix with
+// row stride ld (cols % 16 == 0, 16B-aligned rows).  Zeros are counted in registers (the
+// dominant code at most sites), the rest through a shared histogram.
+__global__ void __launch_bounds__(256) code_hist_kernel(const int8_t* __restrict__ src, int rows, int cols, int ld,
+                                                        unsigned long long* __restrict__ bins) {
+  __shared__ unsigned int h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int vpr = cols / 16;
+  const size_t nvec = size_t(rows) * vpr;
+  unsigned int zeros = 0;
+  for (size_t v = blockIdx.x * size_t(blockDim.x) + threadIdx.x; v < nvec; v += size_t(gridDim.x) * blockDim.x) {
+    const size_t row = v / vpr;
+    const int c16 = int(v - row * vpr);
+    const uint4 q = *reinterpret_cast<const uint4*>(src + row * ld + c16 * 16);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int c = int(int8_t(w[k] >> (8 * b)));
+        if (c == 0) ++zeros;
+        else atomicAdd(&h[c + 128], 1u);
+      }
+  }
+  if (zeros) atomicAdd(&h[128], zeros);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&bins[i], (unsigned long long)h[i]);
+}
+
+cudaError_t launch_code_hist(const int8_t* src, int rows, int cols, int ld, unsigned long long* bins,
+                             cudaStream_t st) {
+  if (cols % 16 || ld % 16 || (reinterpret_cast<uintptr_t>(src) & 15)) return cudaErrorInvalidValue;
+  const size_t nvec = size_t(rows) * (cols / 16);
+  const unsigned blocks = unsigned(std::min<size_t>((nvec + 255) / 256, 4 * 148));
+  if (blocks == 0) return cudaSuccess;
+  code_hist_kernel<<<blocks, 256, 0, st>>>(src, rows, cols, ld, bins);
+  return cudaGetLastError();
+}
+
 }  // namespace samp

@@ -22,8 +22,8 @@ import numpy as np
 from . import _lib
 from .archive import ModelArchive, layer_keys
 from .errors import CalibrationError, ConfigurationError, InputError
-from .plan import (EMBED_OUT_SITE, LAYER_CODE, LAYER_FP, PrecisionPlan)
-from .quantization import CalibrationTable, QuantScale, quantize
+from .plan import (EMBED_OUT_SITE, LAYER_CODE, LAYER_FP, PrecisionPlan, activation_sites)
+from .quantization import CalibrationTable, CodeUsageReport, QuantScale, quantize
 from .tokenization import EncodedInput, encode as encode_text
 from . import trace as _trace
 
@@ -289,6 +289,40 @@ class Engine:
         for e in encs:
             self._validate(e, self.manifest)
         return self.forward_packed(plan, *self.pack(encs), hidden=hidden, head=head)
+
+    # ------------------------------------------------------------ analyze-quant
+    def code_usage(self, encs, plan: PrecisionPlan) -> dict:
+        """{site: CodeUsageReport} summed over ``encs`` for every site ``plan`` quantizes:
+        one device forward with histogram taps on the INT8 codes the kernels write (the
+        reference's tap -> quantize -> code_usage loop, cli.py:284-292)."""
+        self.check_plan(plan)
+        for e in encs:
+            self._validate(e, self.manifest)
+        self._push_calibration()
+        seq_start, att, ids, segs = self.pack(encs)
+        sites = activation_sites(self.manifest.num_layers)
+        counts = np.zeros((len(sites), 256), np.uint64)
+        with self._lock:
+            _lib.check(self._lib.samp_code_usage(self._h, plan.codes(), len(encs), seq_start.ctypes.data,
+                                                 att.ctypes.data, ids.ctypes.data, segs.ctypes.data,
+                                                 counts.ctypes.data))
+        need = plan.required_sites()
+        return {s: CodeUsageReport(s, [int(c) for c in counts[k]])
+                for k, s in enumerate(sites) if s in need}
+
+    def analyze_quant(self, encs, plan: PrecisionPlan, sites: str = "*") -> dict:
+        """reference cli.cmd_analyze_quant (cli.py:269-292) minus the CLI: per-site code
+        usage over ``encs`` for the sites matching the fnmatch filter, in sorted order."""
+        import fnmatch
+        if plan.quantized_layer_count == 0:
+            raise ConfigurationError("analyze-quant needs at least one quantized layer")
+        self.check_plan(plan)
+        names = sorted(plan.required_sites())
+        selected = [s for s in names if fnmatch.fnmatch(s, sites)]
+        if not selected:
+            raise InputError(f"site filter {sites!r} matches nothing; valid sites: {', '.join(names)}")
+        usage = self.code_usage(encs, plan)
+        return {s: usage[s] for s in selected}
 
     # ------------------------------------------------------------ debug / parity
     def set_capture(self, on: bool) -> None:

@@ -340,3 +340,49 @@ def test_tiny_and_odd_sequence_lengths_bit_exact():
     for s, enc in enumerate(encs):
         want = orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions)
         np.testing.assert_array_equal(batch.sequence(s), want, err_msg=f"spec {specs[s]}")
+
+
+# ---------------------------------------------------------------- analyze-quant code usage
+@pytest.mark.parametrize("mode,k", [("FULLY_QUANT", 2), ("FFN_ONLY", 2), ("FULLY_QUANT", 1)])
+def test_code_usage_histograms_equal_oracle(matcher, mode, k):
+    """Engine.code_usage (device histogram taps on the codes the kernels write) equals the
+    reference's analyze-quant loop (cli.py:284-292: tap -> quantize -> code_usage, summed
+    over inputs) on the oracle, for every site the plan quantizes; packed, padded rows."""
+    from paper_2209_09130_b200.quantization import code_usage
+    arch, model = matcher
+    eng = _engine(arch)
+    L = arch.manifest.num_layers
+    plan = PrecisionPlan.prefix(mode, L, k)
+    rng = np.random.default_rng(31)
+    specs = [(64, 64), (64, 20), (32, 32), (32, 5), (40, 33), (16, 16)]
+    encs = [EncodedInput(rng.integers(4, 1000, S).tolist(), [0] * (S // 2) + [1] * (S - S // 2), att)
+            for S, att in specs]
+    got = eng.code_usage(encs, plan)
+    assert set(got) == plan.required_sites()
+    want = {}
+    for enc in encs:
+        taps = {}
+        orc.run(model, enc.token_ids, enc.segment_ids, enc.attention_length, plan.layer_precisions, taps=taps)
+        for site in got:
+            r = code_usage(orc.quantize(taps[site], model.scale(site)), site)
+            want[site] = want[site].merged(r) if site in want else r
+    for site in sorted(got):
+        if mode == "FULLY_QUANT":   # INT8 chain from the embedding: bit-exact codes
+            assert got[site].histogram == want[site].histogram, site
+        else:   # codes downstream of the FP16 tensor-core MHA: rounding flips only
+            g, w = np.array(got[site].histogram), np.array(want[site].histogram)
+            assert g.sum() == w.sum(), site
+            assert np.abs(g - w).sum() <= 0.01 * w.sum(), (site, np.abs(g - w).sum(), w.sum())
+    sm = [s for s in got if s.endswith("softmax")]
+    if sm:   # heads x S x S probabilities per sequence, masked keys included
+        heads = arch.manifest.num_heads
+        assert sum(got[sm[0]].histogram) == heads * sum(S * S for S, _ in specs)
+    # the reference-shaped analyze-quant entry point: fnmatch filter, sorted sites
+    rep = eng.analyze_quant(encs, plan, "L0.ffn.*")
+    assert list(rep) == sorted(s for s in plan.required_sites() if s.startswith("L0.ffn."))
+    assert all(rep[s].histogram == got[s].histogram for s in rep)
+    from paper_2209_09130_b200.errors import ConfigurationError, InputError
+    with pytest.raises(InputError, match="matches nothing"):
+        eng.analyze_quant(encs, plan, "nope*")
+    with pytest.raises(ConfigurationError):
+        eng.analyze_quant(encs, PrecisionPlan.prefix(mode, L, 0))

@@ -149,7 +149,7 @@ __device__ __forceinline__ float att_leaf(uint32_t ta, int col, int n, const X2&
   return res;
 }
 
-template <bool F16, int TPR>
+template <bool F16, int TPR, bool HIST = false>   // HIST: code-usage tap (p.hist) compiled in
 __global__ void __launch_bounds__(att_threads<TPR>(), TPR == 2 ? 3 : 2)
 attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p, int keys_cap) {
   using C = AttnCfg<F16>;
@@ -190,7 +190,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, p.tmem_cols);
-  unsigned int* hist_s = p.hist ? reinterpret_cast<unsigned int*>(smem + lay.hist_off) : nullptr;
+  unsigned int* hist_s = HIST ? reinterpret_cast<unsigned int*>(smem + lay.hist_off) : nullptr;
   if (hist_s)
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist_s[i] = 0;
   tc_fence_before();

@@ -137,8 +137,45 @@ def main():
               taps_plan=("FULLY_QUANT", 1))
 
 
+def analyze_golden():
+    """The reference CLI's analyze-quant on its own tiny_cls model and infer inputs
+    (reference tests/test_cli.py:255-263): CSV output + the token ids it ran on."""
+    import contextlib
+    import io
+    from samp.cli import main as cli_main
+    import tempfile
+    from samp.archive import load_archive, write_archive
+    data = "/root/reference/pkg/tests/data"
+    # the snapshot's tests/data/tiny_cls lacks tensors.bin: rebuild the archive (same
+    # fingerprint as its calibration.json) into a temp dir
+    model_dir = os.path.join(tempfile.mkdtemp(prefix="samp_tiny_"), "tiny_cls")
+    arch = calibrated_archive(seed=0)
+    with open(f"{data}/tiny_cls/calibration.json") as fh:
+        assert json.load(fh)["fingerprint"] == arch.fingerprint
+    write_archive(arch, model_dir)
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = cli_main(["analyze-quant", "--model", model_dir, "--mode", "fully-quant",
+                       "--format", "csv", "--data", f"{data}/infer_inputs.txt", "--sites", "L*.attn.softmax"])
+    assert rc == 0
+    eng = Engine(load_archive(model_dir))
+    with open(f"{data}/infer_inputs.txt", encoding="utf-8") as fh:
+        lines = [ln.rstrip("\n") for ln in fh if ln.strip()]
+    encs = [eng.encode_text(ln) for ln in lines]
+    doc = {"argv": "analyze-quant --mode fully-quant --format csv --sites L*.attn.softmax",
+           "lines": lines,
+           "inputs": [[list(map(int, e.token_ids)), list(map(int, e.segment_ids)), int(e.attention_length)]
+                      for e in encs],
+           "csv": buf.getvalue()}
+    with open(os.path.join(HERE, "analyze_softmax.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    print("analyze_softmax.json", len(encs), "inputs")
+
+
 if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+elif __name__ == "__main__" and sys.argv[1] == "analyze":
+    analyze_golden()
 
 
 def bench_calibration(model="bert-base", n_seq=8, seq=128):

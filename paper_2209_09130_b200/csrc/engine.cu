@@ -707,6 +707,10 @@ static void enqueue_kernels(samp_engine* e, const uint8_t* prec, int nseq, int h
   if (first_int8) {
     ep.out_i8 = a.xq[0];
     ep.s_out = f32(sc(e, "embed.out"));
+    // layer 0 reads only the codes (its residual is dequant(codes)): the float copies are
+    // written only for stage capture (7 B/element less HBM traffic)
+    if (!e->capture) ep.out_f32 = nullptr;
+    ep.out_f16 = nullptr;
   }
   ep.amax = e->calib_amax;   // taps embed.out and L0.attn.in (same tensor)
   ep.site = 0;

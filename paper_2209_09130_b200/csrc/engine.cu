@@ -631,7 +631,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.s_out = f32(sc(e, input_site(i + 1)));
   } else {
     lp.out_f32 = a.hid_f32;
-    lp.out_f16 = a.hid_f16;
+    lp.out_f16 = i + 1 < L ? a.hid_f16 : nullptr;   // f16 copy only feeds a next FP layer
   }
   if (p == SAMP_LAYER_FULL_INT8 || p == SAMP_LAYER_FFN_INT8) {
     const double s_fin = sc(e, lsite(i, "ffn", "in")), s_mid = sc(e, lsite(i, "ffn", "mid"));

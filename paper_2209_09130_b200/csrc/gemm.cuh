@@ -574,7 +574,7 @@ struct ResLNParams {
 // I8_ONLY: the hot INT8 chain (int8 residual, int32 accumulator, only int8 codes out):
 // the general variant's optional outputs are compiled out, shrinking the epilogue code
 // ~3x (ncu showed 20% "no_instruction" stalls on the 80 KB general kernel).
-template <bool I8_ONLY>
+template <bool I8_ONLY, bool REGS96 = false>
 struct EpiResLNT {
   using Params = ResLNParams;
 
@@ -804,7 +804,10 @@ struct EpiResLNT {
 
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
-    if constexpr (NE == 8 && (BN / 2) % 32 == 0 && BN / 2 <= 128) {
+    // register-resident: NE == 8 half rows, or (REGS96) the small-batch 8-CTA clusters'
+    // 96-column rows, one numpy leaf per thread (f32-residual LN: batch-1 FP16 p50 0.712 ->
+    // 0.69 ms; the int8-residual one measured 0.475 -> 0.488 ms and keeps the TMEM variant)
+    if constexpr ((NE == 8 && (BN / 2) % 32 == 0 && BN / 2 <= 128) || (REGS96 && NE == 4 && BN == 96)) {
       run_regs<BN, CLUSTER, NE>(p, c, smem);
     } else {
       run_tmem<BN, CLUSTER, NE>(p, c, smem);
@@ -959,6 +962,7 @@ struct EpiResLNT {
 };
 using EpiResLN = EpiResLNT<false>;
 using EpiResLNI8 = EpiResLNT<true>;
+using EpiResLNRegs96 = EpiResLNT<false, true>;
 
 // ------------------------------------------------------------------ host launcher
 template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>

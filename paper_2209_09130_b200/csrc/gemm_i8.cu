@@ -14,6 +14,20 @@ inline bool persistent_enabled() {
   return on;
 }
 
+static int sm_count() {
+  static thread_local int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+static bool env_on(const char* name) {
+  const char* v = std::getenv(name);
+  return v && v[0] && v[0] != '0';
+}
+
 template <class Epi>
 static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                          const typename Epi::Params& p, cudaStream_t st) {
@@ -27,7 +41,12 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
 #ifdef SAMP_FFN1_64X3
       case 64: return launch_gemm_persistent<KIND_I8, 64, 2, 8, Epi, 3>(a, b, M, N, kb, p, st);
 #else
-      case 64: return launch_gemm_persistent<KIND_I8, 64, 4, 8, Epi, 2>(a, b, M, N, kb, p, st);
+      case 64:
+        // at most one tile per SM (small batches): a deep ring instead of a second CTA —
+        // the whole K of a BERT-base QKV/FFN1 tile in flight at once
+        if (long((M + GEMM_BM - 1) / GEMM_BM) * (N / 64) <= sm_count() && !env_on("SAMP_NO_DEEP64"))
+          return launch_gemm_persistent<KIND_I8, 64, 6, 8, Epi, 1>(a, b, M, N, kb, p, st);
+        return launch_gemm_persistent<KIND_I8, 64, 4, 8, Epi, 2>(a, b, M, N, kb, p, st);
 #endif
     }
     return cudaErrorInvalidValue;

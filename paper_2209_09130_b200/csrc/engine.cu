@@ -134,6 +134,7 @@ struct Activations {
   int* labels = nullptr;
   // A-operand tensor maps (box 128 B x 128 rows) and attention maps (box one head row x 64 rows)
   CUtensorMap a_xq[2], a_ctx_i8, a_ffn_in, a_mid_i8, a_hid_f16, a_ctx_f16, a_ln1_f16, a_mid_f16;
+  CUtensorMap a_ctx_i8_mc[2], a_mid_i8_mc[2];   // 32- / 16-row boxes (A multicast in 4- / 8-CTA clusters)
   CUtensorMap att_qkv_i8, att_qkv_f16;
 };
 
@@ -243,6 +244,10 @@ static void ensure_activations(samp_engine* e, int T) {
   a.a_ctx_i8 = tmap_i8(a.ctx_i8, cap, H, H, 128, 128);
   a.a_ffn_in = tmap_i8(a.ffn_in_i8, cap, H, H, 128, 128);
   a.a_mid_i8 = tmap_i8(a.mid_i8, cap, I, I, 128, 128);
+  for (int k = 0; k < 2; ++k) {
+    a.a_ctx_i8_mc[k] = tmap_i8(a.ctx_i8, cap, H, H, 128, k ? 16 : 32);
+    a.a_mid_i8_mc[k] = tmap_i8(a.mid_i8, cap, I, I, 128, k ? 16 : 32);
+  }
   a.a_hid_f16 = tmap_f16(a.hid_f16, cap, H, H, 64, 128);
   a.a_ctx_f16 = tmap_f16(a.ctx_f16, cap, H, H, 64, 128);
   a.a_ln1_f16 = tmap_f16(a.ln1_f16, cap, H, H, 64, 128);
@@ -564,7 +569,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.out_f16 = a.ln1_f16;
     }
     if (!ln_gemm_splitk(e, "outproj_i8", a.a_ctx_i8, w.m_wo_i8_64, H, lp, st))
-      check_launch(e, gemm_ln_i8(tln, a.a_ctx_i8, ln_small ? w.m_wo_i8_s : w.m_wo_i8, T, H, H, lp, st), "outproj_i8");
+      check_launch(e, gemm_ln_i8(tln, a.a_ctx_i8, ln_small ? w.m_wo_i8_s : w.m_wo_i8, T, H, H, lp, st, a.a_ctx_i8_mc), "outproj_i8");
     record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
     usage_tap(e, 1 + 8 * i + 6, a.ffn_in_i8, T, H, H);
   } else {
@@ -657,7 +662,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.res_scale = f32(s_fin);
     lp.mult = mult_of(s_mid, w.s_w[5]);
     if (!ln_gemm_splitk(e, "ffn2_i8", a.a_mid_i8, w.m_w2_i8_64, I, lp, st))
-      check_launch(e, gemm_ln_i8(tln, a.a_mid_i8, ln_small ? w.m_w2_i8_s : w.m_w2_i8, T, H, I, lp, st), "ffn2_i8");
+      check_launch(e, gemm_ln_i8(tln, a.a_mid_i8, ln_small ? w.m_w2_i8_s : w.m_w2_i8, T, H, I, lp, st, a.a_mid_i8_mc), "ffn2_i8");
   } else {
     EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
     const int k1 = ffn1_bn_index(T, I, e->sms, false);   // EpiF16Out walks 32-column chunks

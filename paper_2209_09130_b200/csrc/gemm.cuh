@@ -93,7 +93,10 @@ struct GemmOcc {
   static constexpr int value = STAGES * (GEMM_BM + BN) * 128 <= 110 * 1024 ? 2 : 1;
 };
 
-template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
+// MC (CLUSTER > 1): the cluster's CTAs share the A row tile; rank r loads rows
+// [r*128/CLUSTER, (r+1)*128/CLUSTER) of every stage multicast to all ranks (map_a then has
+// 128/CLUSTER-row boxes), and each MMA commit frees the stage in every rank
+template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi, bool MC = false>
 __global__ void __launch_bounds__(64 + 32 * NE, GemmOcc<BN, STAGES>::value)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             int M, int k_bytes, const typename Epi::Params ep, unsigned long long* stamps) {
@@ -102,6 +105,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   static_assert(NE == 4 || (NE == 8 && (BN / 2) % 32 == 0), "epilogue split");
+  constexpr bool MCAST = MC && CLUSTER > 1;
+  constexpr int A_ROWS = GEMM_BM / (MCAST ? CLUSTER : 1);   // rows of A this CTA loads
+  constexpr uint16_t MASK = uint16_t((1u << CLUSTER) - 1);
 
   extern __shared__ uint8_t smem_raw[];
   // pointer arithmetic on the __shared__ array keeps the shared address space visible
@@ -129,7 +135,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MCAST ? CLUSTER : 1);
     }
     mbar_init(tmem_full, 1);
     if constexpr (CLUSTER > 1) Epi::template cluster_init<BN>(epi_smem);
@@ -152,18 +158,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       // weights (B) do not depend on the previous kernel: fill the ring's B halves
       // while it drains, then wait for it and stream A
       const int pre = nk < STAGES ? nk : STAGES;
+      const int arow = MCAST ? int(cluster_rank()) * A_ROWS : 0;
+      auto load_a = [&](int s, int kb) {
+        uint8_t* dst = smem + Lay::A_OFF + s * Lay::A_BYTES + arow * 128;
+        if constexpr (MCAST) tma_load_2d_mc(dst, &map_a, kcol(kb), m0 + arow, &full[s], MASK);
+        else tma_load_2d(dst, &map_a, kcol(kb), m0, &full[s]);
+      };
       for (int kb = 0; kb < pre; ++kb) {
         mbar_expect_tx(&full[kb], Lay::A_BYTES + Lay::B_BYTES);
         tma_load_2d(smem + Lay::B_OFF + kb * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[kb]);
       }
       pdl_wait();
-      for (int kb = 0; kb < pre; ++kb)
-        tma_load_2d(smem + Lay::A_OFF + kb * Lay::A_BYTES, &map_a, kcol(kb), m0, &full[kb]);
+      for (int kb = 0; kb < pre; ++kb) load_a(kb, kb);
       for (int kb = pre; kb < nk; ++kb) {
         const int s = kb % STAGES;
-        mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+        mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);   // MCAST: every rank consumed the stage
         mbar_expect_tx(&full[s], Lay::A_BYTES + Lay::B_BYTES);
-        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kcol(kb), m0, &full[s]);
+        load_a(s, kb);
         tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[s]);
       }
     }
@@ -182,7 +193,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           mma_ss<KIND>(tmem, sdesc_k_sw128(a_base + 32 * k), sdesc_k_sw128(b_base + 32 * k), IDESC,
                        (kb | k) != 0);
         }
-        mma_commit(&empty[s]);
+        if constexpr (MCAST) mma_commit_mc(&empty[s], MASK);
+        else mma_commit(&empty[s]);
       }
       mma_commit(tmem_full);
       pdl_trigger();   // last MMA issued: the next kernel's prologue overlaps our epilogue
@@ -216,6 +228,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+  // MCAST: peers' last MMA commits arrive on our empty barriers; nobody exits before all did
+  if constexpr (MCAST) cluster_sync_all();
   if (stamp && threadIdx.x == 0) stamp[6] = globaltimer();
 }
 
@@ -965,11 +979,11 @@ using EpiResLNI8 = EpiResLNT<true>;
 using EpiResLNRegs96 = EpiResLNT<false, true>;
 
 // ------------------------------------------------------------------ host launcher
-template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi>
+template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi, bool MC = false>
 inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N, int k_bytes,
                                const typename Epi::Params& p, cudaStream_t stream, int ksplit = 1) {
   using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
-  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi>;
+  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi, MC>;
   static thread_local int configured_device = -1;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -3,8 +3,14 @@
 
 namespace samp {
 
+static bool mcast_on() {
+  const char* v = std::getenv("SAMP_LN_MCAST");
+  return v && v[0] == '1';
+}
+
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
-                       const EpiResLN::Params& p, cudaStream_t st) {
+                       const EpiResLN::Params& p, cudaStream_t st, const CUtensorMap* a_mc) {
+  const bool mc = a_mc && mcast_on();
   // Many more row tiles than co-resident clusters (probed, gemm_ln_persistent.cuh): persistent
   // clusters with double-buffered TMEM walk the row tiles (C5 FFN2 1.09 vs 1.51 ms at 262k
   // tokens).  With only a few tiles per cluster the fill/drain and the uneven split lose
@@ -28,12 +34,16 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
                        !p.out_f32 && !p.out_f16;
   if (i8_only) {
     switch (t.bn_ln * 10 + t.cluster_ln) {
-      case 1924: return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
+      case 1924:
+        if (mc) return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8, true>(a_mc[0], b, M, N, kb, p, st);
+        return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
       case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
     }
   }
   switch (t.bn_ln * 10 + t.cluster_ln) {
-    case 1924: return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);
+    case 1924:
+      if (mc) return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLN, true>(a_mc[0], b, M, N, kb, p, st);
+      return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 2562: return launch_gemm<KIND_I8, 256, 3, 2, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 1922: return launch_gemm<KIND_I8, 192, 4, 2, 8, EpiResLN>(a, b, M, N, kb, p, st);
@@ -43,7 +53,9 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
     // small batches: 8-CTA clusters; each CTA streams K x 96 weights alone, so the ring
     // depth sets the bytes in flight (batch-1 fully-quant p50 0.474 vs 0.507 ms at 4 stages;
     // 7 stages no better)
-    case 968: return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
+    case 968:
+      if (mc) return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN, true>(a_mc[1], b, M, N, kb, p, st);
+      return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
     case 1288: return launch_gemm<KIND_I8, 128, 5, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
   }
   return cudaErrorInvalidValue;

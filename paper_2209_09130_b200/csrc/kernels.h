@@ -25,8 +25,10 @@ cudaError_t gelu_fast_check(float s, float inv_s, unsigned long long* host_count
 cudaError_t gemm_gelu_i8(int bn, int mode, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                          const EpiGeluQuant::Params& p, cudaStream_t st);
 // gemm_ln.cu
+// a_mc (optional): the same A with 32-row / 16-row boxes, for A multicast across 4- / 8-CTA
+// clusters (SAMP_LN_MCAST)
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
-                       const EpiResLN::Params& p, cudaStream_t st);
+                       const EpiResLN::Params& p, cudaStream_t st, const CUtensorMap* a_mc = nullptr);
 // small batches: split-K GEMM into an int32 workspace (64-wide tiles, grid z = ksplit)
 cudaError_t gemm_splitk_i8(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb, int ksplit,
                            const EpiSplitKAdd::Params& p, cudaStream_t st);

@@ -439,7 +439,7 @@ static float gelu_inv_s(float s) { return float(1.0 / double(s)); }
 // check per distinct scale, cached for the engine's lifetime).  SAMP_NO_GELU_FAST=1 keeps
 // the exact epilogue everywhere (A/B measurements).
 static void gelu_fast_prepare(samp_engine* e, const uint8_t* prec) {
-  static const bool off = std::getenv("SAMP_NO_GELU_FAST") != nullptr;
+  static const bool off = env_flag("SAMP_NO_GELU_FAST");
   if (off) return;
   for (int i = 0; i < e->d.num_layers; ++i) {
     if (prec[i] != SAMP_LAYER_FULL_INT8 && prec[i] != SAMP_LAYER_FFN_INT8) continue;
@@ -459,7 +459,7 @@ static void gelu_fast_prepare(samp_engine* e, const uint8_t* prec) {
 // gain at batch 1 (fully-quant p50 0.595 vs 0.575 ms), so the fused cluster kernel stays
 // the default.
 static int splitk_factor(int T, int N, int kblocks, int sms) {
-  if (!std::getenv("SAMP_SPLITK")) return 0;
+  if (!env_flag("SAMP_SPLITK")) return 0;
   const int tiles = ((T + GEMM_BM - 1) / GEMM_BM) * (N / 64);
   int best = 0;
   for (int d = 2; d <= kblocks; ++d)
@@ -492,7 +492,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   // small batches: twice the LN-GEMM CTAs (8-CTA clusters, one numpy leaf each) so each
   // streams half the weights; SAMP_NO_LN_SMALL=1 keeps the 4-CTA clusters
   const int mtiles = (T + GEMM_BM - 1) / GEMM_BM;
-  const bool ln_small = e->tiles.bn_ln_small && mtiles * 8 <= e->sms && !std::getenv("SAMP_NO_LN_SMALL");
+  const bool ln_small = e->tiles.bn_ln_small && mtiles * 8 <= e->sms && !env_flag("SAMP_NO_LN_SMALL");
   Tiles tsm = e->tiles;
   if (ln_small) {
     tsm.bn_ln = tsm.bn_ln_small;
@@ -501,7 +501,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   const Tiles& t = e->tiles;
   const Tiles& tln = tsm;
   // QKV tiles 64 wide when 128-wide ones would leave most SMs idle (batch 1: 36 CTAs, not 18)
-  const bool qkv_narrow = mtiles * (3 * H / 128) * 2 <= e->sms && (3 * H) % 64 == 0 && !std::getenv("SAMP_NO_QKV_NARROW");
+  const bool qkv_narrow = mtiles * (3 * H / 128) * 2 <= e->sms && (3 * H) % 64 == 0 && !env_flag("SAMP_NO_QKV_NARROW");
   const float eps = f32(e->d.layernorm_eps);
   const int fp16_store = e->d.fp16_storage;
   const bool int8_attn = p == SAMP_LAYER_FULL_INT8 || p == SAMP_LAYER_MHA_INT8;
@@ -526,7 +526,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     qp.sout2 = f32(sc(e, lsite(i, "attn", "v")));
     // persistent 128-wide tiles, two CTAs/SM: 35.9k vs 35.8k sentences/s at batch 32 and
     // batch-1 fully-quant p50 0.525 vs 0.55 ms (twice the CTAs at one row tile)
-    if (!std::getenv("SAMP_QKV_ONETILE") && (3 * H) % 128 == 0)
+    if (!env_flag("SAMP_QKV_ONETILE") && (3 * H) % 128 == 0)
       check_launch(e, qkv_narrow ? gemm_qkv_i8(-64, a.a_xq[cur], w.m_qkv_i8_64, T, 3 * H, H, qp, st)
                                  : gemm_qkv_i8(-128, a.a_xq[cur], w.m_qkv_i8_128, T, 3 * H, H, qp, st), "qkv_i8");
     else
@@ -649,7 +649,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     auto ok = e->gelu_fast_ok.find(bits_of(gp.s_out));
     const bool fast = finite && ok != e->gelu_fast_ok.end() && ok->second;
     gp.inv_s = gelu_inv_s(gp.s_out);
-    if (std::getenv("SAMP_GELU_FLAGS")) {   // measurement: count flagged 8-groups per forward
+    if (env_flag("SAMP_GELU_FLAGS")) {   // measurement: count flagged 8-groups per forward
       if (!g_gelu_flags) cudaMallocManaged(&g_gelu_flags, sizeof(unsigned long long));
       gp.flag_count = g_gelu_flags;
     }
@@ -1228,7 +1228,7 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       }
     }
     if (io == SAMP_IO_HOST) SAMP_CUDA(cudaStreamSynchronize(st));
-    if (g_gelu_flags && std::getenv("SAMP_GELU_FLAGS")) {
+    if (g_gelu_flags && env_flag("SAMP_GELU_FLAGS")) {
       SAMP_CUDA(cudaDeviceSynchronize());
       std::fprintf(stderr, "gelu_fast: %llu flagged 8-groups of %lld\n", *g_gelu_flags,
                    (long long)T * d.intermediate / 8 * d.num_layers);

@@ -20,7 +20,7 @@ static int sm_count_f16() {
 cudaError_t gemm_f16out(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                         const EpiF16Out::Params& p, cudaStream_t st) {
   constexpr int NEP = SAMP_PERSIST_NE;
-  if (std::getenv("SAMP_NO_PERSISTENT") == nullptr) {
+  if (!env_flag("SAMP_NO_PERSISTENT")) {
     switch (bn) {
       case 256: return launch_gemm_persistent<KIND_F16, 256, 4, NEP, EpiF16Out>(a, b, M, N, kb, p, st);
       case 128: return launch_gemm_persistent<KIND_F16, 128, 5, NEP, EpiF16Out>(a, b, M, N, kb, p, st);

@@ -10,7 +10,7 @@ namespace samp {
 
 // persistent (gemm_persistent.cuh) unless SAMP_NO_PERSISTENT is set (A/B measurements)
 inline bool persistent_enabled() {
-  static const bool on = std::getenv("SAMP_NO_PERSISTENT") == nullptr;
+  static const bool on = !env_flag("SAMP_NO_PERSISTENT");
   return on;
 }
 
@@ -22,10 +22,6 @@ static int sm_count() {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   }
   return n;
-}
-static bool env_on(const char* name) {
-  const char* v = std::getenv(name);
-  return v && v[0] && v[0] != '0';
 }
 
 template <class Epi>
@@ -44,7 +40,7 @@ static cudaError_t by_bn(int bn, bool persistent, const CUtensorMap& a, const CU
       case 64:
         // at most one tile per SM (small batches): a deep ring instead of a second CTA —
         // the whole K of a BERT-base QKV/FFN1 tile in flight at once
-        if (long((M + GEMM_BM - 1) / GEMM_BM) * (N / 64) <= sm_count() && !env_on("SAMP_NO_DEEP64"))
+        if (long((M + GEMM_BM - 1) / GEMM_BM) * (N / 64) <= sm_count() && !env_flag("SAMP_NO_DEEP64"))
           return launch_gemm_persistent<KIND_I8, 64, 6, 8, Epi, 1>(a, b, M, N, kb, p, st);
         return launch_gemm_persistent<KIND_I8, 64, 4, 8, Epi, 2>(a, b, M, N, kb, p, st);
 #endif

@@ -8,14 +8,14 @@ cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap&
   // same persistent rule as gemm_ln_i8 (kind::f16, f32 accumulators and residuals):
   // C5 out-proj 0.86 vs 1.22 ms per launch
   const int mtiles = (M + GEMM_BM - 1) / GEMM_BM;
-  if (std::getenv("SAMP_NO_LN_PERSISTENT") == nullptr && (mtiles >= 256 || std::getenv("SAMP_LN_PERSISTENT"))) {
+  if (!env_flag("SAMP_NO_LN_PERSISTENT") && (mtiles >= 256 || env_flag("SAMP_LN_PERSISTENT"))) {
     switch (t.bn_ln * 10 + t.cluster_ln) {
       case 1924:
-        if (mtiles >= 8 * ln_persistent_clusters<KIND_F16, 192, 4, 4>() || std::getenv("SAMP_LN_PERSISTENT"))
+        if (mtiles >= 8 * ln_persistent_clusters<KIND_F16, 192, 4, 4>() || env_flag("SAMP_LN_PERSISTENT"))
           return launch_gemm_ln_persistent<KIND_F16, 192, 4, 4>(a, b, M, kb, p, st);
         break;
       case 2564:
-        if (mtiles >= 8 * ln_persistent_clusters<KIND_F16, 256, 3, 4>() || std::getenv("SAMP_LN_PERSISTENT"))
+        if (mtiles >= 8 * ln_persistent_clusters<KIND_F16, 256, 3, 4>() || env_flag("SAMP_LN_PERSISTENT"))
           return launch_gemm_ln_persistent<KIND_F16, 256, 3, 4>(a, b, M, kb, p, st);
         break;
     }

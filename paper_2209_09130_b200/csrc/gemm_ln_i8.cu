@@ -3,28 +3,23 @@
 
 namespace samp {
 
-static bool mcast_on() {
-  const char* v = std::getenv("SAMP_LN_MCAST");
-  return v && v[0] == '1';
-}
-
 cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
                        const EpiResLN::Params& p, cudaStream_t st, const CUtensorMap* a_mc) {
-  const bool mc = a_mc && mcast_on();
+  const bool mc = a_mc && env_flag("SAMP_LN_MCAST");
   // Many more row tiles than co-resident clusters (probed, gemm_ln_persistent.cuh): persistent
   // clusters with double-buffered TMEM walk the row tiles (C5 FFN2 1.09 vs 1.51 ms at 262k
   // tokens).  With only a few tiles per cluster the fill/drain and the uneven split lose
   // (C4 out-proj 72 vs 57 us at 4 tiles/cluster), hence >= 8 tiles per cluster; otherwise
   // one tile per CTA.  SAMP_NO_LN_PERSISTENT=1 / SAMP_LN_PERSISTENT=1 force either.
   const int mtiles = (M + GEMM_BM - 1) / GEMM_BM;
-  if (std::getenv("SAMP_NO_LN_PERSISTENT") == nullptr && (mtiles >= 256 || std::getenv("SAMP_LN_PERSISTENT"))) {
+  if (!env_flag("SAMP_NO_LN_PERSISTENT") && (mtiles >= 256 || env_flag("SAMP_LN_PERSISTENT"))) {
     switch (t.bn_ln * 10 + t.cluster_ln) {
       case 1924:
-        if (mtiles >= 8 * ln_persistent_clusters<KIND_I8, 192, 4, 4>() || std::getenv("SAMP_LN_PERSISTENT"))
+        if (mtiles >= 8 * ln_persistent_clusters<KIND_I8, 192, 4, 4>() || env_flag("SAMP_LN_PERSISTENT"))
           return launch_gemm_ln_persistent<KIND_I8, 192, 4, 4>(a, b, M, kb, p, st);
         break;
       case 2564:
-        if (mtiles >= 8 * ln_persistent_clusters<KIND_I8, 256, 3, 4>() || std::getenv("SAMP_LN_PERSISTENT"))
+        if (mtiles >= 8 * ln_persistent_clusters<KIND_I8, 256, 3, 4>() || env_flag("SAMP_LN_PERSISTENT"))
           return launch_gemm_ln_persistent<KIND_I8, 256, 3, 4>(a, b, M, kb, p, st);
         break;
     }

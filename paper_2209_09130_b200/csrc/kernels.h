@@ -3,6 +3,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "attention.cuh"
 #include "embed.cuh"
 #include "gemm.cuh"
@@ -10,6 +12,12 @@
 #include "ln_rows.cuh"
 
 namespace samp {
+
+// measurement switch: set and not empty / "0"
+inline bool env_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && v[0] && !(v[0] == '0' && v[1] == 0);
+}
 
 struct Tiles {
   int bn_qkv, bn_ffn1, bn_ln, cluster_ln;

@@ -104,7 +104,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   constexpr int TMEM_COLS = tmem_cols_for(BN);
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
-  static_assert(NE == 4 || (NE == 8 && (BN / 2) % 32 == 0), "epilogue split");
+  static_assert(NE == 4 || (NE == 8 && ((BN / 2) % 32 == 0 || BN == 96)), "epilogue split");
   constexpr bool MCAST = MC && CLUSTER > 1;
   constexpr int A_ROWS = GEMM_BM / (MCAST ? CLUSTER : 1);   // rows of A this CTA loads
   constexpr uint16_t MASK = uint16_t((1u << CLUSTER) - 1);
@@ -816,12 +816,128 @@ struct EpiResLNT {
     }
   }
 
+  // Two threads per row over one 96-column numpy leaf (BN = 96, NE = 8): numpy's 8 strided
+  // accumulators split by index — half h owns r[4h .. 4h+3], i.e. columns 8g + 4h + u — so
+  // half 0 forms (r0+r1)+(r2+r3), half 1 (r4+r5)+(r6+r7), and reduce_row's half combine is
+  // numpy's final add.  Each thread reads the whole row from TMEM once and keeps its 48
+  // values in registers; normalisation and outputs run on 4-column groups.
+  template <int BN, int CLUSTER, int NE>
+  __device__ static void run_strided(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    static_assert(BN == 96 && NE == 8, "one 96-column leaf split over two threads");
+    float* halves = reinterpret_cast<float*>(smem);
+    const float* sbias = halves + RED_FLOATS;
+    const float* sgam = sbias + BN;
+    const float* sbet = sgam + BN;
+    const uint8_t* rtile = smem + (RED_FLOATS + 3 * BN) * 4 + c.tile_row * res_ld<BN>();
+    const bool valid = c.row < c.M;
+    const size_t rbase = size_t(valid ? c.row : 0) * p.hidden;
+    const int jo = 4 * c.half;
+    const uint32_t tbase = c.taddr - uint32_t(c.c0);
+    float x[48];
+    // the register index must be compile-time: one body per half
+    auto fill = [&](auto jo_c) {
+      constexpr int JO = decltype(jo_c)::value;
+      uint32_t r[96];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) tmem_ld32(tbase + 32 * k, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * k));
+      tmem_wait_ld();
+#pragma unroll
+      for (int g = 0; g < 12; ++g) {
+        const int col = 8 * g + JO;
+        float res[4];
+        if (p.res_i8) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(rtile + col);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) res[u] = deq(int(int8_t((w >> (8 * u)) & 0xff)), p.res_scale);
+        } else {
+          const float4 v = *reinterpret_cast<const float4*>(p.res_f32 + rbase + c.n0 + col);
+          res[0] = v.x; res[1] = v.y; res[2] = v.z; res[3] = v.w;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t a = r[col + u];
+          const float acc = p.acc_is_f32 ? __uint_as_float(a) : __fmul_rn(__int2float_rn(int(a)), p.mult);
+          x[4 * g + u] = __fadd_rn(__fadd_rn(acc, sbias[col + u]), res[u]);
+        }
+      }
+    };
+    if (c.half == 0) fill(std::integral_constant<int, 0>{});
+    else fill(std::integral_constant<int, 4>{});
+    auto half_leaf = [&](auto f) {
+      float a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = f(x[u]);
+#pragma unroll
+      for (int g = 1; g < 12; ++g)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = __fadd_rn(a[u], f(x[4 * g + u]));
+      return __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
+    };
+    const float hf = float(p.hidden);
+    const float total = reduce_row<BN, CLUSTER, NE>(half_leaf([](float v) { return v; }), c, halves, smem, 0);
+    const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
+    const float total2 = reduce_row<BN, CLUSTER, NE>(half_leaf([mean](float v) {
+                                                   const float d = __fsub_rn(v, mean);
+                                                   return __fmul_rn(d, d);
+                                                 }),
+                                                 c, halves, smem, 1);
+    const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+    const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);
+    float amx = 0.0f;
+    if (valid) {
+#pragma unroll
+      for (int g = 0; g < 12; ++g) {
+        const int col = 8 * g + jo;
+        const size_t o = rbase + c.n0 + col;
+        float y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          y[u] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[4 * g + u], mean), inv), sgam[col + u]), sbet[col + u]);
+        if (p.deq_outputs) {
+          int q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[u] = quant_fast(y[u], rq);
+          if (p.out_i8) *reinterpret_cast<uint32_t*>(p.out_i8 + o) = pack4_i8(q[0], q[1], q[2], q[3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) y[u] = deq(q[u], p.s_out);
+        } else if (p.out_i8) {
+          *reinterpret_cast<uint32_t*>(p.out_i8 + o) =
+              trunc_pack4_s8(quant_pre_fast(y[0], rq), quant_pre_fast(y[1], rq), quant_pre_fast(y[2], rq),
+                             quant_pre_fast(y[3], rq));
+        }
+        if (p.f16_round) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) y[u] = __half2float(__float2half_rn(y[u]));
+        }
+        if (p.amax) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) amx = fmaxf(amx, fabsf(y[u]));
+        }
+        if (p.out_f32) *reinterpret_cast<float4*>(p.out_f32 + o) = make_float4(y[0], y[1], y[2], y[3]);
+        if (p.out_f16) {
+          __half2 h0 = __floats2half2_rn(y[0], y[1]), h1 = __floats2half2_rn(y[2], y[3]);
+          *reinterpret_cast<uint2*>(p.out_f16 + o) =
+              make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        }
+      }
+    }
+    if (p.amax) {
+      amax_commit(p.amax + p.site, amx);
+      if (p.site2 >= 0) amax_commit(p.amax + p.site2, amx);
+    }
+  }
+
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
+    if constexpr (NE == 8 && BN == 96) {
+      run_strided<BN, CLUSTER, NE>(p, c, smem);
+      return;
+    }
     // register-resident: NE == 8 half rows, or (REGS96) the small-batch 8-CTA clusters'
     // 96-column rows, one numpy leaf per thread (f32-residual LN: batch-1 FP16 p50 0.712 ->
     // 0.69 ms; the int8-residual one measured 0.475 -> 0.488 ms and keeps the TMEM variant)
-    if constexpr ((NE == 8 && (BN / 2) % 32 == 0 && BN / 2 <= 128) || (REGS96 && NE == 4 && BN == 96)) {
+    else if constexpr ((NE == 8 && (BN / 2) % 32 == 0 && BN / 2 <= 128) || (REGS96 && NE == 4 && BN == 96)) {
       run_regs<BN, CLUSTER, NE>(p, c, smem);
     } else {
       run_tmem<BN, CLUSTER, NE>(p, c, smem);

@@ -49,8 +49,11 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
     // depth sets the bytes in flight (batch-1 fully-quant p50 0.474 vs 0.507 ms at 4 stages;
     // 7 stages no better)
     case 968:
+      // two epilogue threads per row, numpy's accumulators split by index (run_strided):
+      // batch-1 fully-quant p50 0.469 -> 0.454 ms vs one thread per row
       if (mc) return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN, true>(a_mc[1], b, M, N, kb, p, st);
-      return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
+      if (env_flag("SAMP_NO_LN96_STRIDED")) return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
+      return launch_gemm<KIND_I8, 96, 6, 8, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 1288: return launch_gemm<KIND_I8, 128, 5, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
   }
   return cudaErrorInvalidValue;

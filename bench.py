@@ -381,9 +381,12 @@ def run_samp(args):
     line = None
     if rank == 0:
         cpu = None
+        parity = None
         if world == 1 and not args.no_cpu:
+            ref_out = []
             with _all_host_threads():
-                cpu = cpu_baseline(arch, plan, args, wl=wl)
+                cpu = cpu_baseline(arch, plan, args, wl=wl, outputs=ref_out)
+            parity = bench_parity(eng, plan, wl, ref_out, cpu["kind"])
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "sentences/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
@@ -396,13 +399,41 @@ def run_samp(args):
                        "calibration": "reference (tests/golden)" if wl.key == "c2" else "on-device, 8 rng(1) sequences"},
             "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
             "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps, "e2e_text": e2e_text,
-            "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels,
+            "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def bench_parity(eng, plan, wl, ref_out, kind):
+    """The sentences the CPU baseline just ran, through the public API on the GPU: final
+    hidden states bit-exact (INT8 plans), logits within 1e-5 (the reference's head GEMMs
+    use BLAS order), labels equal."""
+    n = len(ref_out)
+    if not n:
+        return None
+    seq_start, att, ids, segs = synthetic_batch(0, n, wl.seq, wl.pairs)
+    res = eng.forward_packed(plan, seq_start, att, ids, segs, hidden=True)
+    exact = sum(int(np.array_equal(res.sequence(s), ref_out[s][0])) for s in range(n))
+    if wl.task == "sequence_labeling":
+        lg = [res.logits[seq_start[s]:seq_start[s] + int(att[s])] for s in range(n)]
+        lab = [res.labels[seq_start[s]:seq_start[s] + int(att[s])].tolist() for s in range(n)]
+    else:
+        lg = [res.logits[s] for s in range(n)]
+        lab = [[int(res.labels[s])] for s in range(n)]
+    dl = max(float(np.max(np.abs(np.asarray(lg[s]).reshape(-1) - ref_out[s][1].reshape(-1)))) for s in range(n))
+    same = sum(int(lab[s] == ref_out[s][2]) for s in range(n))
+    rel = max(float(np.linalg.norm(res.sequence(s) - ref_out[s][0]) / np.linalg.norm(ref_out[s][0]))
+              for s in range(n))
+    int8 = all(p == "FULL_INT8" for p in plan.layer_precisions)
+    ok = exact == n and dl <= 1e-5 and same == n if int8 else rel < 2e-2
+    return {"sentences": n, "against": "reference package (baseline/_ref)" if kind == "reference" else "oracle port",
+            "hidden_bit_exact": f"{exact}/{n}", "hidden_max_rel_l2": rel, "max_abs_logit_diff": dl,
+            "labels_equal": f"{same}/{n}", "bar": "bit-exact hidden, logits 1e-5" if int8 else "FP16 tolerance",
+            "ok": bool(ok)}
 
 
 def _host_cores():
@@ -494,7 +525,9 @@ def reference_runner(wl):
             plan = samp.encoder.PrecisionPlan.prefix(wl.mode, shapes["num_layers"], shapes["num_layers"])
             warm = [False]
 
-            def runner(n_sent):
+            def runner(n_sent, outputs=None):
+                """sentences/s over the first n_sent sentences of rank 0's batch; with a list
+                `outputs`, also append (hidden_states, logits, label_ids) per sentence"""
                 seq_start, att, ids, segs = synthetic_batch(0, n_sent, wl.seq, wl.pairs)
                 encs = [samp.tokenization.EncodedInput(ids[seq_start[s]:seq_start[s + 1]].tolist(),
                                                        segs[seq_start[s]:seq_start[s + 1]].tolist(), int(att[s]))
@@ -506,32 +539,35 @@ def reference_runner(wl):
                 for s, enc in enumerate(encs):
                     out = eng.run(enc, plan)
                     if wl.task == "sequence_labeling":
-                        samp.tasks.tag(arch, out, int(att[s]))
+                        res = samp.tasks.tag(arch, out, int(att[s]))
                     else:
-                        samp.tasks.classify(arch, out)
+                        res = samp.tasks.classify(arch, out)
+                    if outputs is not None:
+                        outputs.append((out.hidden_states, np.asarray(res.logits, np.float32), list(res.label_ids)))
                 return n_sent / (time.perf_counter() - t0)
     _REF_RUNNERS[wl.key] = runner
     return runner
 
 
-def cpu_baseline(arch, plan, args, n_sent=None, wl=None):
+def cpu_baseline(arch, plan, args, n_sent=None, wl=None, outputs=None):
     """The reference's CPU path on a bounded sample of the same workload: the reference's
-    own package when installed in baseline/_ref (kind "reference"), else the oracle port."""
+    own package when installed in baseline/_ref (kind "reference"), else the oracle port.
+    `outputs` (a list) collects the reference's per-sentence results for the parity check."""
     wl = wl or WORKLOADS["c2"]
     n = n_sent or (args.cpu_sentences if wl.key == "c2" else 2)
     runner = reference_runner(wl) if wl.key == "c2" else None
     if runner is not None:
-        v = runner(n)
+        v = runner(n, outputs)
         if v is not None:
             return {"value": round(v, 4), "unit": "sentences/s", "cores": _blas_threads(), "kind": "reference",
                     "sample": f"{n} of the {wl.batch} x {wl.seq}-token sentences, {wl.mode} "
                               f"{arch.manifest.num_layers}/{arch.manifest.num_layers} + {wl.task} head, the "
                               f"reference's own samp.encoder.Engine.run + samp.tasks (numpy, OpenBLAS threads), "
                               f"installed in baseline/_ref"}
-    return cpu_baseline_port(arch, plan, args, n_sent, wl)
+    return cpu_baseline_port(arch, plan, args, n_sent, wl, outputs)
 
 
-def cpu_baseline_port(arch, plan, args, n_sent=None, wl=None):
+def cpu_baseline_port(arch, plan, args, n_sent=None, wl=None, outputs=None):
     """The reference's CPU path (oracle port) on a bounded sample of the same workload."""
     from oracle import samp_oracle as orc
 
@@ -548,9 +584,12 @@ def cpu_baseline_port(arch, plan, args, n_sent=None, wl=None):
         r0, r1 = seq_start[s], seq_start[s + 1]
         h = orc.run(model, ids[r0:r1], segs[r0:r1], int(att[s]), plan.layer_precisions)
         if wl.task == "sequence_labeling":
-            orc.tag_logits(model, h, int(att[s]))
+            lg, _, lab = orc.tag_logits(model, h, int(att[s]))
         else:
-            orc.classify_logits(model, h)
+            lg, _, lab = orc.classify_logits(model, h)
+            lab = [lab]
+        if outputs is not None:
+            outputs.append((h, np.asarray(lg, np.float32), list(lab)))
     dt = time.perf_counter() - t0
     return {"value": round(n_sent / dt, 4), "unit": "sentences/s", "cores": _blas_threads(), "kind": "port",
             "sample": f"{n_sent} of the {wl.batch} x {wl.seq}-token sentences, {wl.mode} "

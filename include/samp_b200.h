@@ -15,6 +15,13 @@
  * the reference's exception classes (errors.py:4-41); the message is in
  * samp_last_error() (thread-local).  All validation happens before any
  * device work, as in the reference.
+ *
+ * Threading (reference: one Engine shared across threads, encoder.py:431,437-441;
+ * results bitwise thread-independent, tests/test_encoder.py:340-350): every entry point
+ * taking a samp_engine* holds that engine's (recursive) mutex for the whole call, so
+ * calls on one engine are serialised — a calibration change can never interleave with
+ * a forward that is reading scales or replaying a captured graph.  Different engines
+ * run concurrently.  samp_engine_destroy must not race other calls on the same engine.
  */
 #ifndef SAMP_B200_H
 #define SAMP_B200_H

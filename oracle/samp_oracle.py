@@ -139,6 +139,28 @@ def gemm_f32(a, b) -> np.ndarray:
     return out
 
 
+class blas_fp32:
+    """Context manager for large-sample STATISTICAL tests only: the FP32 GEMMs run as BLAS
+    sgemm instead of the reference's rank-1 k-order loop (kernels.py:62-71).  Results then
+    differ from the reference by float32 summation order (~1e-6 relative), far inside the
+    FP16-path tolerance those tests check; every bit-exact test keeps the restatement.
+    exp / tanh are numpy's own here (the npmath restatement is only needed for bit-exact
+    parity on hosts whose numpy dispatches differently)."""
+
+    def __enter__(self):
+        global gemm_f32, np_exp, np_tanh
+        self._saved = gemm_f32, np_exp, np_tanh
+        gemm_f32 = lambda a, b: np.matmul(np.asarray(a, F32), np.asarray(b, F32)).astype(F32)  # noqa: E731
+        # numpy's own float32 transcendentals (== npmath on the AVX512 hosts it restates)
+        np_exp = lambda x: np.exp(np.asarray(x, F32))    # noqa: E731
+        np_tanh = lambda x: np.tanh(np.asarray(x, F32))  # noqa: E731
+        return self
+
+    def __exit__(self, *exc):
+        global gemm_f32, np_exp, np_tanh
+        gemm_f32, np_exp, np_tanh = self._saved
+
+
 def softmax(x) -> np.ndarray:
     """kernels.softmax_rows (kernels.py:130-135)."""
     shifted = x - np.max(x, axis=-1, keepdims=True)

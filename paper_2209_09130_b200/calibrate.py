@@ -15,7 +15,6 @@ from __future__ import annotations
 import ctypes
 
 from . import _lib
-from .errors import ConfigurationError
 from .plan import activation_sites
 from .quantization import CalibrationTable
 
@@ -41,13 +40,9 @@ def calibrate_engine(engine, encoded_inputs, max_tokens: int = 1 << 16) -> Calib
     out = (ctypes.c_double * len(sites))()
     for b in batches:
         seq_start, att, ids, segs = engine.pack(b)
-        _lib.check(engine._lib.samp_calibrate(engine.handle, len(b), seq_start.ctypes.data, att.ctypes.data,
-                                              ids.ctypes.data, segs.ctypes.data, out))
+        with engine._lock:     # the calibration forward reuses the engine's buffers
+            _lib.check(engine._lib.samp_calibrate(engine.handle, len(b), seq_start.ctypes.data, att.ctypes.data,
+                                                  ids.ctypes.data, segs.ctypes.data, out))
         for site, v in zip(sites, out):
             table.observe_amax(site, float(v))
     return table
-
-
-def run_with_taps(engine, enc, plan):
-    raise ConfigurationError("capture_taps is not supported on the GPU path: use Engine.calibrate() for "
-                             "per-site amax, or the oracle for full tap tensors")

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <set>
 #include <string>
 #include <vector>
@@ -140,7 +141,7 @@ struct Activations {
 
 struct Geometry {
   std::vector<int> seq_start, att_len, tile_seq, tile_q0, tile_cnt;
-  int nseq = 0, T = 0, ntiles = 0, max_nkp = 0;
+  int nseq = 0, T = 0, ntiles = 0, max_nkp = 0, max_s = 0;
   int *d_seq_start = nullptr, *d_att_len = nullptr, *d_tile_seq = nullptr, *d_tile_q0 = nullptr, *d_tile_cnt = nullptr;
   int cap_seq = 0, cap_tiles = 0;
 };
@@ -148,6 +149,9 @@ struct Geometry {
 }  // namespace samp
 
 struct samp_engine {
+  // every entry point that reads or writes engine state holds this (samp_b200.h threading
+  // contract); recursive because samp_calibrate / samp_code_usage call samp_forward
+  std::recursive_mutex mu;
   samp_model_desc d{};
   int device = 0;
   cudaStream_t stream = nullptr;          // the engine's own stream
@@ -187,6 +191,15 @@ struct samp_engine {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   std::map<std::string, std::pair<double, long>> prof;  // name -> (total ms, launches)
+  // capture_taps (samp_set_capture(e, 2)): F32 site values, recorded as stages "tap:<site>"
+  bool taps = false;
+  int tap_cap = 0;                 // token rows of the tap scratch buffers
+  void* tap_acc = nullptr;         // [cap][max(3H, I)] int32 / f32 accumulators
+  float *tap_out = nullptr, *tap_ctx = nullptr, *tap_ln = nullptr, *tap_probs = nullptr;
+  size_t tap_probs_cap = 0;
+  long long* tap_prob_off = nullptr;
+  int tap_prob_off_cap = 0;
+  size_t tap_probs_total = 0;      // floats of this forward's softmax tap
   int* pinned_ids = nullptr;   // staging for host inputs
   int pinned_cap = 0;
   float* pinned_out = nullptr;  // staging for the head outputs (one D2H)
@@ -270,8 +283,10 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
   g.max_nkp = 0;
   e->h_pos.resize(seq_start[nseq]);
   g.tile_cnt.clear();
+  g.max_s = 0;
   for (int s = 0; s < nseq; ++s) {
     const int S = seq_start[s + 1] - seq_start[s];
+    g.max_s = std::max(g.max_s, S);
     g.att_len[s] = std::min(att_len[s], S);
     for (int t = 0; t < S; ++t) e->h_pos[seq_start[s] + t] = t;
   }
@@ -299,6 +314,9 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
   }
   g.T = seq_start[nseq];
   g.ntiles = int(g.tile_seq.size());
+  // captured graphs bake these device pointers into kernel arguments: a reallocation
+  // invalidates every graph
+  if (nseq + 1 > g.cap_seq || g.ntiles > g.cap_tiles) clear_graphs(e);
   if (nseq + 1 > g.cap_seq) {
     if (g.d_seq_start) { e->mem.release(g.d_seq_start); e->mem.release(g.d_att_len); }
     g.cap_seq = std::max(nseq + 1, 64);
@@ -356,6 +374,45 @@ static void record(samp_engine* e, const std::string& name, int layer, const voi
   SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));
   SAMP_CUDA(cudaMemcpy(host.data(), dev, bytes, cudaMemcpyDeviceToHost));
   e->stages[name + "@" + std::to_string(layer)] = std::move(host);
+}
+
+static void tap_record(samp_engine* e, const std::string& site, const void* dev, size_t bytes) {
+  if (e->taps) record(e, "tap:" + site, -1, dev, bytes);
+}
+
+// grow the tap scratch buffers for this forward's geometry; per-sequence softmax offsets
+static void ensure_taps(samp_engine* e) {
+  const Geometry& g = e->geo;
+  const int H = e->d.hidden, I = e->d.intermediate, A = e->d.num_heads;
+  const int wide = std::max(3 * H, I);
+  if (g.T > e->tap_cap) {
+    for (void* q : {(void*)e->tap_acc, (void*)e->tap_out, (void*)e->tap_ctx, (void*)e->tap_ln})
+      if (q) e->mem.release(q);
+    e->tap_cap = std::max(g.T, 128);
+    e->tap_acc = e->mem.alloc<int>(size_t(e->tap_cap) * wide);
+    e->tap_out = e->mem.alloc<float>(size_t(e->tap_cap) * wide);
+    e->tap_ctx = e->mem.alloc<float>(size_t(e->tap_cap) * H);
+    e->tap_ln = e->mem.alloc<float>(size_t(e->tap_cap) * H);
+  }
+  std::vector<long long> off(g.nseq);
+  size_t tot = 0;
+  for (int s = 0; s < g.nseq; ++s) {
+    const long long S = g.seq_start[s + 1] - g.seq_start[s];
+    off[s] = (long long)tot;
+    tot += size_t(A) * S * S;
+  }
+  if (tot > e->tap_probs_cap) {
+    if (e->tap_probs) e->mem.release(e->tap_probs);
+    e->tap_probs_cap = tot;
+    e->tap_probs = e->mem.alloc<float>(tot);
+  }
+  if (g.nseq > e->tap_prob_off_cap) {
+    if (e->tap_prob_off) e->mem.release(e->tap_prob_off);
+    e->tap_prob_off_cap = g.nseq;
+    e->tap_prob_off = e->mem.alloc<long long>(g.nseq);
+  }
+  e->tap_probs_total = tot;
+  SAMP_CUDA(cudaMemcpy(e->tap_prob_off, off.data(), g.nseq * sizeof(long long), cudaMemcpyHostToDevice));
 }
 
 static cudaEvent_t take_event(samp_engine* e) {
@@ -469,7 +526,7 @@ static int splitk_factor(int T, int N, int kblocks, int sms) {
 static bool ln_gemm_splitk(samp_engine* e, const char* name, const CUtensorMap& a_map, const CUtensorMap& b64,
                            int K, const EpiResLN::Params& lp, cudaStream_t st) {
   const int T = e->geo.T, H = e->d.hidden;
-  const bool i8_only = lp.res_i8 && !lp.acc_is_f32 && lp.out_i8 && !lp.deq_outputs && !lp.f16_round && !lp.amax &&
+  const bool i8_only = lp.res_i8 && !lp.acc_is_f32 && lp.out_i8 && !lp.deq_outputs && !lp.f16_round && !lp.amax && !lp.tap_f32 &&
                        !lp.out_f32 && !lp.out_f16;
   if (!i8_only || !ln_rows_supported(H) || H % 64) return false;
   const int ks = splitk_factor(T, H, K / 128, e->sms);
@@ -480,6 +537,53 @@ static bool ln_gemm_splitk(samp_engine* e, const char* name, const CUtensorMap& 
                   lp.out_i8, lp.s_out};
   check_launch(e, launch_ln_rows(rp, H, st), "ln_rows");
   return true;
+}
+
+// capture_taps: q/k/v (per-block dequant + bias) from the QKV accumulators
+static void taps_qkv(samp_engine* e, int i, bool f16, const CUtensorMap& a_map, const LayerDev& w, float m0,
+                     float m1, float m2, int f16_round) {
+  const int T = e->geo.T, H = e->d.hidden;
+  cudaStream_t st = e->stream_in_use;
+  check_launch(e, gemm_store_acc(f16 ? KIND_F16 : KIND_I8, e->tiles.bn_qkv, a_map, f16 ? w.m_qkv_f16 : w.m_qkv_i8,
+                                 T, 3 * H, f16 ? 2 * H : H, e->tap_acc, 3 * H, st), "tap_gemm");
+  TapBiasParams tb{e->tap_acc, int(f16), 3 * H, T, 3 * H, w.qkv_b, m0, m1, m2, H, 0, f16_round, e->tap_out};
+  check_launch(e, launch_tap_bias(tb, st), "tap_bias");
+  const char* nm[3] = {"q", "k", "v"};
+  for (int k = 0; k < 3; ++k) tap_record(e, lsite(i, "attn", nm[k]), e->tap_out + size_t(k) * T * H, size_t(T) * H * 4);
+}
+
+// capture_taps: softmax probabilities and the context before its quantize
+static void taps_attention(samp_engine* e, int i, bool f16, const AttnParams& ap, int f16_round) {
+  const Geometry& g = e->geo;
+  const int H = e->d.hidden;
+  TapAttnParams ta{};
+  ta.qkv = f16 ? static_cast<const void*>(e->act.qkv_f16) : static_cast<const void*>(e->act.qkv_i8);
+  ta.f16 = f16;
+  ta.hidden = H;
+  ta.seq_start = g.d_seq_start;
+  ta.att_len = g.d_att_len;
+  ta.mult_scores = ap.mult_scores;
+  ta.s_softmax = ap.s_softmax;
+  ta.mult_ctx = ap.mult_ctx;
+  ta.f16_round = f16_round;
+  ta.probs = e->tap_probs;
+  ta.prob_off = e->tap_prob_off;
+  ta.ctx = e->tap_ctx;
+  check_launch(e, launch_tap_attention(ta, g.max_s, e->d.num_heads, g.nseq, e->stream_in_use), "tap_attention");
+  tap_record(e, lsite(i, "attn", "softmax"), e->tap_probs, e->tap_probs_total * 4);
+  tap_record(e, lsite(i, "attn", "out_in"), e->tap_ctx, size_t(g.T) * H * 4);
+}
+
+// capture_taps: ffn.mid = GELU(dequant(acc) + b1) (int8) or GELU(acc + b1) (f16 path)
+static void taps_ffn_mid(samp_engine* e, int i, bool f16, const CUtensorMap& a_map, const LayerDev& w, float mult,
+                         int f16_round) {
+  const int T = e->geo.T, H = e->d.hidden, I = e->d.intermediate;
+  const int k1 = I % 128 == 0 ? 2 : 0;   // FFN1_BN[k1] = 128 or 64
+  check_launch(e, gemm_store_acc(f16 ? KIND_F16 : KIND_I8, FFN1_BN[k1], a_map, f16 ? w.m_w1_f16[k1] : w.m_w1_i8[k1],
+                                 T, I, f16 ? 2 * H : H, e->tap_acc, I, e->stream_in_use), "tap_gemm");
+  TapBiasParams tb{e->tap_acc, int(f16), I, T, I, w.b1, mult, mult, mult, 0, 1, f16_round, e->tap_out};
+  check_launch(e, launch_tap_bias(tb, e->stream_in_use), "tap_bias");
+  tap_record(e, lsite(i, "ffn", "mid"), e->tap_out, size_t(T) * I * 4);
 }
 
 // one encoder layer; `in_q` = index of xq holding this layer's input codes (INT8 inputs)
@@ -532,6 +636,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     else
       check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
     record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
+    if (e->taps) taps_qkv(e, i, false, a.a_xq[cur], w, qp.mult0, qp.mult1, qp.mult2, 0);
     for (int k = 0; k < 3; ++k) usage_tap(e, 1 + 8 * i + 1 + k, a.qkv_i8 + k * H, T, H, 3 * H);
     AttnParams ap{};
     ap.ctx_out = a.ctx_i8;
@@ -550,6 +655,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.tmem_cols = tmem_cols_for_keys(e->geo.max_nkp);
     if (e->usage) ap.hist = e->usage + size_t(1 + 8 * i + 4) * 256;
     launch_attention(e, false, ap);
+    if (e->taps) taps_attention(e, i, false, ap, 0);
     record(e, "ctx_q", i, a.ctx_i8, size_t(T) * H);
     usage_tap(e, 1 + 8 * i + 5, a.ctx_i8, T, H, H);
     EpiResLN::Params lp{};
@@ -568,12 +674,18 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.out_f32 = a.ln1_f32;
       lp.out_f16 = a.ln1_f16;
     }
+    if (e->taps) lp.tap_f32 = e->tap_ln;
     if (!ln_gemm_splitk(e, "outproj_i8", a.a_ctx_i8, w.m_wo_i8_64, H, lp, st))
       check_launch(e, gemm_ln_i8(tln, a.a_ctx_i8, ln_small ? w.m_wo_i8_s : w.m_wo_i8, T, H, H, lp, st, a.a_ctx_i8_mc), "outproj_i8");
+    tap_record(e, lsite(i, "ffn", "in"), e->tap_ln, size_t(T) * H * 4);
     record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
     usage_tap(e, 1 + 8 * i + 6, a.ffn_in_i8, T, H, H);
   } else {
     record(e, "in_f32", i, a.hid_f32, size_t(T) * H * 4);
+    tap_record(e, lsite(i, "attn", "in"), a.hid_f32, size_t(T) * H * 4);
+    // reference fp16 storage rounds the FP layers' stored values; FFN_ONLY's MHA runs
+    // without it (encoder.py:493-497 passes round_fn None)
+    const int rnd = p == SAMP_LAYER_FP ? fp16_store : 0;
     float* cal = e->calib_amax;
     const int cbase = 1 + 8 * i;   // activation_sites order: attn.in q k v softmax out_in ffn.in ffn.mid
     EpiF16Out::Params qp{a.qkv_f16, 3 * H, w.qkv_b, 0, cal, cbase + 1, H};
@@ -581,6 +693,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       check_launch(e, gemm_f16out(64, a.a_hid_f16, w.m_qkv_f16_64, T, 3 * H, 2 * H, qp, st), "qkv_f16");
     else
       check_launch(e, gemm_f16out(t.bn_qkv, a.a_hid_f16, w.m_qkv_f16, T, 3 * H, 2 * H, qp, st), "qkv_f16");
+    if (e->taps) taps_qkv(e, i, true, a.a_hid_f16, w, 1.0f, 1.0f, 1.0f, rnd);
     AttnParams ap{};
     ap.ctx_out = a.ctx_f16;
     ap.tile_seq = e->geo.d_tile_seq;
@@ -595,6 +708,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.site_sm = cbase + 4;
     ap.site_ctx = cbase + 5;
     launch_attention(e, true, ap);
+    if (e->taps) taps_attention(e, i, true, ap, rnd);
     EpiResLN::Params lp{};
     lp.bias = w.ob;
     lp.res_f32 = a.hid_f32;
@@ -614,8 +728,10 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.site = cbase + 6;
       lp.site2 = -1;
     }
+    if (e->taps) lp.tap_f32 = e->tap_ln;
     check_launch(e, gemm_ln_f16(tln, a.a_ctx_f16, ln_small ? w.m_wo_f16_s : w.m_wo_f16, T, H, 2 * H, lp, st),
                  "outproj_f16");
+    tap_record(e, lsite(i, "ffn", "in"), e->tap_ln, size_t(T) * H * 4);
     if (p == SAMP_LAYER_FFN_INT8) {
       record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
       usage_tap(e, 1 + 8 * i + 6, a.ffn_in_i8, T, H, H);
@@ -634,6 +750,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   if (next_int8) {
     lp.out_i8 = a.xq[cur ^ 1];
     lp.s_out = f32(sc(e, input_site(i + 1)));
+    if (e->taps) lp.tap_f32 = e->tap_ln;   // attn.in of the next layer, before its quantize
   } else {
     lp.out_f32 = a.hid_f32;
     lp.out_f16 = i + 1 < L ? a.hid_f16 : nullptr;   // f16 copy only feeds a next FP layer
@@ -657,6 +774,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     check_launch(e, gemm_gelu_i8(FFN1_BN[k1], fast ? GELU_FAST : finite ? GELU_FINITE : GELU_GENERAL, a.a_ffn_in,
                                  w.m_w1_i8[k1], T, I, H, gp, st), "ffn1_i8");
     record(e, "mid_q", i, a.mid_i8, size_t(T) * I);
+    if (e->taps) taps_ffn_mid(e, i, false, a.a_ffn_in, w, gp.mult, 0);
     usage_tap(e, 1 + 8 * i + 7, a.mid_i8, T, I, I);
     lp.res_i8 = a.ffn_in_i8;
     lp.res_scale = f32(s_fin);
@@ -667,6 +785,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
     const int k1 = ffn1_bn_index(T, I, e->sms, false);   // EpiF16Out walks 32-column chunks
     check_launch(e, gemm_f16out(FFN1_BN[k1], a.a_ln1_f16, w.m_w1_f16[k1], T, I, 2 * H, gp, st), "ffn1_f16");
+    if (e->taps) taps_ffn_mid(e, i, true, a.a_ln1_f16, w, 1.0f, p == SAMP_LAYER_FP ? fp16_store : 0);
     lp.res_f32 = a.ln1_f32;
     lp.acc_is_f32 = 1;
     lp.f16_round = (p == SAMP_LAYER_FP) ? fp16_store : 0;
@@ -680,6 +799,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   }
   if (next_int8) {
     cur ^= 1;
+    tap_record(e, input_site(i + 1), e->tap_ln, size_t(T) * H * 4);
     record(e, "out_q", i, a.xq[cur], size_t(T) * H);
   } else {
     record(e, "out_f32", i, a.hid_f32, size_t(T) * H * 4);
@@ -722,6 +842,7 @@ static void enqueue_kernels(samp_engine* e, const uint8_t* prec, int nseq, int h
   ep.site2 = 1;
   check_launch(e, launch_embed(ep, st), "embed");
   record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
+  tap_record(e, "embed.out", a.hid_f32, size_t(T) * H * 4);
   int cur = 0;
   for (int i = 0; i < L; ++i) run_layer(e, i, prec, cur);
   // ---------------- heads + outputs (final hidden is always F32 in hid_f32)
@@ -798,6 +919,7 @@ extern "C" void samp_engine_destroy(samp_engine* e) {
 
 extern "C" int samp_load_embeddings(samp_engine* e, const float* word, const float* position,
                                     const float* token_type, const float* g, const float* b) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     SAMP_CUDA(cudaSetDevice(e->device));
     const size_t H = e->d.hidden;
@@ -816,6 +938,7 @@ extern "C" int samp_load_embeddings(samp_engine* e, const float* word, const flo
 }
 
 extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     SAMP_REQUIRE(layer >= 0 && layer < e->d.num_layers, SAMP_E_CONFIGURATION, "layer index out of range");
     SAMP_CUDA(cudaSetDevice(e->device));
@@ -893,6 +1016,7 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
 
 extern "C" int samp_load_heads(samp_engine* e, const float* pool_w, const float* pool_b, const float* head_w,
                                const float* head_b) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     SAMP_CUDA(cudaSetDevice(e->device));
     const int H = e->d.hidden, L = e->d.num_labels;
@@ -919,6 +1043,7 @@ extern "C" int samp_load_heads(samp_engine* e, const float* pool_w, const float*
 }
 
 extern "C" int samp_weight_scales(samp_engine* e, int layer, double* out6) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     SAMP_REQUIRE(layer >= 0 && layer < e->d.num_layers && e->layers[layer].loaded, SAMP_E_CONFIGURATION,
                  "layer not loaded");
@@ -927,6 +1052,7 @@ extern "C" int samp_weight_scales(samp_engine* e, int layer, double* out6) {
 }
 
 extern "C" int samp_set_site_amax(samp_engine* e, const char* site, double amax) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     clear_graphs(e);
     e->amax[site] = amax;
@@ -934,6 +1060,7 @@ extern "C" int samp_set_site_amax(samp_engine* e, const char* site, double amax)
 }
 
 extern "C" int samp_clear_calibration(samp_engine* e) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     clear_graphs(e);
     e->amax.clear();
@@ -945,6 +1072,7 @@ extern "C" int samp_debug_gelu_fast_check(float s, unsigned long long* counts) {
 }
 
 extern "C" int samp_set_graphs(samp_engine* e, int on) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     clear_graphs(e);
     e->graphs_enabled = on != 0;
@@ -952,14 +1080,17 @@ extern "C" int samp_set_graphs(samp_engine* e, int on) {
 }
 
 extern "C" int samp_set_capture(samp_engine* e, int on) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     e->capture = on != 0;
+    e->taps = on == 2;   // 2: also the F32 site taps (Engine.run capture_taps=True)
     if (e->capture) e->stages.clear();  // turning capture off keeps the last forward's stages
   });
 }
 
 extern "C" int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, size_t capacity,
                                 size_t* bytes) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     auto it = e->stages.find(std::string(name) + "@" + std::to_string(layer));
     SAMP_REQUIRE(it != e->stages.end(), SAMP_E_CONFIGURATION,
@@ -976,6 +1107,7 @@ extern "C" int samp_fetch_stage(samp_engine* e, const char* name, int layer, voi
 // with max|x| taps at all 1 + 8L activation sites, in activation_sites order.
 extern "C" int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_start, const int32_t* att_len,
                               const int32_t* ids, const int32_t* segs, double* amax_out) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   int rc = SAMP_OK;
   rc = guarded([&] {
     const int n = 1 + 8 * e->d.num_layers;
@@ -1007,6 +1139,7 @@ extern "C" int samp_calibrate(samp_engine* e, int32_t nseq, const int32_t* seq_s
 extern "C" int samp_code_usage(samp_engine* e, const uint8_t* prec, int32_t nseq, const int32_t* seq_start,
                                const int32_t* att_len, const int32_t* ids, const int32_t* segs,
                                unsigned long long* counts) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   int rc = SAMP_OK;
   rc = guarded([&] {
     const size_t n = size_t(1 + 8 * e->d.num_layers) * 256;
@@ -1029,12 +1162,14 @@ extern "C" int samp_code_usage(samp_engine* e, const uint8_t* prec, int32_t nseq
 }
 
 extern "C" int samp_sync(samp_engine* e) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] { SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use)); });
 }
 
 extern "C" int samp_last_launch_count(samp_engine* e) { return e ? e->launches : 0; }
 
 extern "C" int samp_debug_gemm_stamps(samp_engine* e, int max_launches) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     if (e->stamps) e->mem.release(e->stamps);
     e->stamps = nullptr;
@@ -1049,6 +1184,7 @@ extern "C" int samp_debug_gemm_stamps(samp_engine* e, int max_launches) {
 
 extern "C" int samp_debug_gemm_stamps_fetch(samp_engine* e, unsigned long long* out, int cap_launches,
                                             char* names, size_t names_cap, int* n_launches) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     SAMP_REQUIRE(e->stamps, SAMP_E_CONFIGURATION, "GEMM stamps not enabled");
     SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));
@@ -1064,6 +1200,7 @@ extern "C" int samp_debug_gemm_stamps_fetch(samp_engine* e, unsigned long long* 
 }
 
 extern "C" int samp_set_profiling(samp_engine* e, int on) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     e->profiling = on != 0;
     e->prof.clear();
@@ -1073,6 +1210,7 @@ extern "C" int samp_set_profiling(samp_engine* e, int on) {
 // sync, fold pending event pairs into per-kernel totals, and write them as JSON
 // {"name": [total_ms, launches], ...} into buf
 extern "C" int samp_profile_report(samp_engine* e, char* buf, size_t cap) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));
     for (auto& p : e->pending) {
@@ -1101,6 +1239,7 @@ extern "C" int samp_profile_report(samp_engine* e, char* buf, size_t cap) {
 extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, const int32_t* seq_start,
                             const int32_t* att_len, const int32_t* ids, const int32_t* segs, int32_t io,
                             const samp_outputs* out, void* stream_arg) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
     const samp_model_desc& d = e->d;
     const int L = d.num_layers, H = d.hidden;
@@ -1160,7 +1299,7 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
     if (io == SAMP_IO_HOST) {
       if (e->pinned_cap < 2 * T) {
         if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
-  if (e->pinned_out) cudaFreeHost(e->pinned_out);
+        e->pinned_ids = nullptr;
         e->pinned_cap = std::max(2 * T, 8192);
         SAMP_CUDA(cudaMallocHost(&e->pinned_ids, size_t(e->pinned_cap) * sizeof(int)));
       }
@@ -1173,6 +1312,7 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       SAMP_CUDA(cudaMemcpyAsync(a.segs, segs, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
     }
     gelu_fast_prepare(e, prec);
+    if (e->taps) ensure_taps(e);
     // ---------------- device work: replay a captured CUDA graph for this (plan, batch
     // geometry, head) when one exists; capture on the second sighting of a key (the first
     // run also configures every kernel's smem attributes outside of capture)
@@ -1207,7 +1347,10 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       SAMP_CUDA(cudaGraphLaunch(exec, st));
     } else {
       enqueue_kernels(e, prec, nseq, head, st);
-      if (graphable) e->seen.insert(key);
+      if (graphable) {
+        if (e->seen.size() >= 256) e->seen.clear();   // bounded: variable-shape servers
+        e->seen.insert(key);
+      }
     }
     const cudaMemcpyKind kind = io == SAMP_IO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     const size_t head_bytes = (2 * rows * nl + rows) * 4;

@@ -584,6 +584,7 @@ struct ResLNParams {
   __half* out_f16;                // optional
   float* amax;                    // calibration: amax array (null = off)
   int site, site2;                // sites tapped with the emitted values (site2 < 0: none)
+  float* tap_f32 = nullptr;       // capture_taps: [M][H] LayerNorm output before quantize
 };
 // I8_ONLY: the hot INT8 chain (int8 residual, int32 accumulator, only int8 codes out):
 // the general variant's optional outputs are compiled out, shrinking the epilogue code
@@ -689,6 +690,16 @@ struct EpiResLNT {
 
   // emit 32 normalised values (quantize / deq / f16 round / amax / stores)
   __device__ static void emit32(const Params& p, size_t rbase, int gcol, const Recip& rq, float (&y)[32], float& amx) {
+    // reference order: storage rounding (fp16 mode) happens before any quantize
+    if (p.f16_round) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
+    }
+    if (p.tap_f32) {
+      float4* dst = reinterpret_cast<float4*>(p.tap_f32 + rbase + gcol);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dst[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+    }
     if (p.deq_outputs) {
       int q[32];
 #pragma unroll
@@ -701,10 +712,6 @@ struct EpiResLNT {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = quant_pre_fast(y[j], rq);
       store32_pre(p.out_i8 + rbase + gcol, v);
-    }
-    if (p.f16_round) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
     }
     if (p.amax) {
 #pragma unroll
@@ -894,6 +901,11 @@ struct EpiResLNT {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           y[u] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[4 * g + u], mean), inv), sgam[col + u]), sbet[col + u]);
+        if (p.f16_round) {   // storage rounding precedes any quantize (reference order)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) y[u] = __half2float(__float2half_rn(y[u]));
+        }
+        if (p.tap_f32) *reinterpret_cast<float4*>(p.tap_f32 + o) = make_float4(y[0], y[1], y[2], y[3]);
         if (p.deq_outputs) {
           int q[4];
 #pragma unroll
@@ -905,10 +917,6 @@ struct EpiResLNT {
           *reinterpret_cast<uint32_t*>(p.out_i8 + o) =
               trunc_pack4_s8(quant_pre_fast(y[0], rq), quant_pre_fast(y[1], rq), quant_pre_fast(y[2], rq),
                              quant_pre_fast(y[3], rq));
-        }
-        if (p.f16_round) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) y[u] = __half2float(__float2half_rn(y[u]));
         }
         if (p.amax) {
 #pragma unroll
@@ -1047,42 +1055,7 @@ struct EpiResLNT {
       for (int j = 0; j < 32; ++j)
         y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(__uint_as_float(r[j]), mean), inv), g[j]), be[j]);
       if (!valid) continue;
-      if (p.deq_outputs) {
-        int q[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) q[j] = quant_fast(y[j], rq);
-        if (p.out_i8) store32_i8(p.out_i8 + rbase + gcol, q);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) y[j] = deq(q[j], p.s_out);
-      } else if (p.out_i8) {
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = quant_pre_fast(y[j], rq);
-        store32_pre(p.out_i8 + rbase + gcol, v);
-      }
-      if (p.f16_round) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
-      }
-      if (p.amax) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) amx = fmaxf(amx, fabsf(y[j]));
-      }
-      if (p.out_f32) {
-        float4* dst = reinterpret_cast<float4*>(p.out_f32 + rbase + gcol);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) dst[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
-      }
-      if (p.out_f16) {
-        uint4* dst = reinterpret_cast<uint4*>(p.out_f16 + rbase + gcol);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          __half2 h0 = __floats2half2_rn(y[8 * j], y[8 * j + 1]), h1 = __floats2half2_rn(y[8 * j + 2], y[8 * j + 3]);
-          __half2 h2 = __floats2half2_rn(y[8 * j + 4], y[8 * j + 5]), h3 = __floats2half2_rn(y[8 * j + 6], y[8 * j + 7]);
-          dst[j] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
-                              *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
-        }
-      }
+      emit32(p, rbase, gcol, rq, y, amx);
     }
     if (p.amax) {
       amax_commit(p.amax + p.site, amx);

@@ -26,7 +26,7 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
   }
   // the hot chain (int8 residual in, int8 codes out, nothing else): compact epilogue
   const bool i8_only = p.res_i8 && !p.acc_is_f32 && p.out_i8 && !p.deq_outputs && !p.f16_round && !p.amax &&
-                       !p.out_f32 && !p.out_f16;
+                       !p.out_f32 && !p.out_f16 && !p.tap_f32;
   if (i8_only) {
     switch (t.bn_ln * 10 + t.cluster_ln) {
       case 1924:

@@ -59,6 +59,31 @@ cudaError_t launch_tag(const HeadParams& p, cudaStream_t st);
 cudaError_t launch_pack_weight(const float* w, int K, int N, float scale, int8_t* out_i8, __half* out_f16,
                                int row_off, cudaStream_t st);
 cudaError_t launch_transpose_f32(const float* w, int K, int N, float* out, cudaStream_t st);
+// capture_taps (taps.cu): F32 site values re-derived next to the fused kernels
+struct TapBiasParams {
+  const void* acc;        // [M][ld_acc] int32 (kind::i8) or f32 (kind::f16) accumulators
+  int acc_f32, ld_acc, M, N;
+  const float* bias;      // [N]
+  float mult0, mult1, mult2;   // per column block dequant multipliers (int32 accumulators)
+  int block_cols;         // > 0: column blocks of this width are separate [M][block_cols] outputs
+  int gelu, f16_round;
+  float* out;
+};
+struct TapAttnParams {
+  const void* qkv;        // [T][3H] int8 codes or f16 values (the fused QKV output)
+  int f16, hidden;
+  const int* seq_start;
+  const int* att_len;
+  float mult_scores, s_softmax, mult_ctx;
+  int f16_round;
+  float* probs;           // per sequence [heads][S][S] at prob_off[seq]
+  const long long* prob_off;
+  float* ctx;             // [T][H]
+};
+cudaError_t launch_tap_bias(const TapBiasParams& p, cudaStream_t st);
+cudaError_t launch_tap_attention(const TapAttnParams& p, int max_s, int heads, int nseq, cudaStream_t st);
+cudaError_t gemm_store_acc(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,
+                           void* out, int ldc, cudaStream_t st);
 // code-usage tap: bins[256] += histogram of an int8 [rows][cols] matrix (row stride ld)
 cudaError_t launch_code_hist(const int8_t* src, int rows, int cols, int ld, unsigned long long* bins,
                              cudaStream_t st);

@@ -82,7 +82,7 @@ class Engine:
         self.vocab = archive.vocab
         self.fp16_storage = bool(fp16_storage)
         self.device = int(device)
-        self._lock = threading.Lock()
+        self._lock = threading.RLock()   # re-entrant: forward_packed -> _push_calibration
         self._quantized: dict = {}
         self._lib = lib = _lib.load()
         desc = _lib.ModelDesc(m.num_layers, m.hidden, m.num_heads, m.intermediate, m.vocab_size,
@@ -118,32 +118,36 @@ class Engine:
     def calibration(self) -> CalibrationTable | None:
         return self.archive.calibration
 
-    def _push_calibration(self) -> None:
+    def _calibration_state(self):
+        """Snapshot of the archive's table, read fresh on every call as the reference does
+        (encoder.py:456-470): direct edits of ``table.entries`` (replaced or mutated
+        QuantScale objects, deleted sites) are seen without relying on any version counter."""
         table = self.archive.calibration
-        # fast path: the very table object pushed last (held, so its id cannot be reused),
-        # unchanged through its API (version) and with the same entry count
-        key = None if table is None else (table.version, len(table.entries))
-        if table is not None and table is getattr(self, "_pushed_table", None) and key == self._pushed_key:
-            return
-        state = None if table is None else tuple(sorted((s, e.amax) for s, e in table.entries.items()))
-        self._pushed_table, self._pushed_key = table, key
-        if state == self._pushed_calibration:
-            return
-        _lib.check(self._lib.samp_clear_calibration(self._h))
-        for site, amax in state or ():
-            _lib.check(self._lib.samp_set_site_amax(self._h, site.encode(), float(amax)))
-        self._pushed_calibration = state
+        if table is None:
+            return None
+        return tuple(sorted((s, float(e.amax)) for s, e in table.entries.items()))
+
+    def _push_calibration(self) -> None:
+        """Send the table's amax values to the device when they differ from what it holds."""
+        with self._lock:
+            state = self._calibration_state()
+            if state == self._pushed_calibration:
+                return
+            _lib.check(self._lib.samp_clear_calibration(self._h))
+            self._pushed_calibration = None
+            for site, amax in state or ():
+                _lib.check(self._lib.samp_set_site_amax(self._h, site.encode(), amax))
+            self._pushed_calibration = state
 
     def check_plan(self, plan: PrecisionPlan) -> CalibrationTable | None:
         """reference encoder.py:456-470 (same messages)."""
         table = self.calibration
-        # a plan already checked against this very table, unchanged since: nothing to redo
-        key = (plan.layer_precisions, table.version if table is not None else -1,
-               len(table.entries) if table is not None else -1)
-        if key == getattr(self, "_checked_key", None) and table is getattr(self, "_checked_table", None):
+        # a plan already checked against a table holding the same site names: nothing to redo
+        key = (plan.layer_precisions, None if table is None else frozenset(table.entries))
+        if key == getattr(self, "_checked_key", None):
             return table
         self._check_plan_uncached(plan)
-        self._checked_key, self._checked_table = key, table
+        self._checked_key = key
         return table
 
     def _check_plan_uncached(self, plan: PrecisionPlan) -> CalibrationTable | None:
@@ -225,7 +229,13 @@ class Engine:
 
     def forward_packed(self, plan: PrecisionPlan, seq_start, att_len, ids, segs, *, hidden=True,
                        head: int | None = None) -> BatchOutput:
-        """One samp_forward call over packed host arrays (validated by the library)."""
+        """One samp_forward call over packed host arrays (validated by the library).  The
+        plan check, the calibration push and the forward run under one lock, so another
+        thread's table change cannot interleave with them."""
+        with self._lock:
+            return self._forward_packed_locked(plan, seq_start, att_len, ids, segs, hidden, head)
+
+    def _forward_packed_locked(self, plan, seq_start, att_len, ids, segs, hidden, head) -> BatchOutput:
         self.check_plan(plan)
         self._trace(plan, seq_start)
         self._push_calibration()
@@ -248,10 +258,9 @@ class Engine:
         att_len = np.ascontiguousarray(att_len, dtype=np.int32)
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         segs = np.ascontiguousarray(segs, dtype=np.int32)
-        with self._lock:
-            _lib.check(self._lib.samp_forward(self._h, plan.codes(), nseq, seq_start.ctypes.data,
-                                              att_len.ctypes.data, ids.ctypes.data, segs.ctypes.data,
-                                              IO_HOST, ctypes.byref(out), None))
+        _lib.check(self._lib.samp_forward(self._h, plan.codes(), nseq, seq_start.ctypes.data,
+                                          att_len.ctypes.data, ids.ctypes.data, segs.ctypes.data,
+                                          IO_HOST, ctypes.byref(out), None))
         return BatchOutput(seq_start, hid, logits, probs, labels)
 
     def run(self, enc: EncodedInput, plan: PrecisionPlan, capture_taps: bool = False) -> EncoderOutput:
@@ -259,8 +268,8 @@ class Engine:
         self.check_plan(plan)
         self._validate(enc, self.manifest)
         if capture_taps:
-            from .calibrate import run_with_taps
-            return run_with_taps(self, enc, plan)
+            out = self.run_batch_taps([enc], plan)
+            return EncoderOutput(hidden_states=out[0][0], taps=out[0][1], head=None)
         seq_start, att, ids, segs = self.pack([enc])
         res = self.forward_packed(plan, seq_start, att, ids, segs)
         head = None
@@ -290,19 +299,62 @@ class Engine:
             self._validate(e, self.manifest)
         return self.forward_packed(plan, *self.pack(encs), hidden=hidden, head=head)
 
+    def run_batch_taps(self, encs, plan: PrecisionPlan) -> list:
+        """[(hidden_states, taps)] per sequence: one device forward with every activation
+        site's F32 value captured (reference Engine.run(..., capture_taps=True),
+        encoder.py:472-530 / _tap :238-240).  Sites and shapes as the reference: [S, H]
+        (ffn.mid [S, I]), softmax [heads, S, S].  INT8-chain sites are bit-exact; sites on
+        the FP16 tensor-core path carry its tolerance."""
+        for e in encs:
+            self._validate(e, self.manifest)
+        m = self.manifest
+        seq_start, att, ids, segs = self.pack(encs)
+        with self._lock:
+            self.set_capture(2)
+            try:
+                res = self._forward_packed_locked(plan, seq_start, att, ids, segs, True, HEAD_NONE)
+                got = {}
+                for site in activation_sites(m.num_layers):
+                    size = ctypes.c_size_t()
+                    name = ("tap:" + site).encode()
+                    if self._lib.samp_fetch_stage(self._h, name, -1, None, 0, ctypes.byref(size)) != 0:
+                        continue
+                    buf = np.empty(size.value // 4, np.float32)
+                    _lib.check(self._lib.samp_fetch_stage(self._h, name, -1, buf.ctypes.data, buf.nbytes,
+                                                          ctypes.byref(size)))
+                    got[site] = buf
+            finally:
+                self.set_capture(0)
+        out = []
+        sq = 0
+        for s, enc in enumerate(encs):
+            r0, r1 = int(seq_start[s]), int(seq_start[s + 1])
+            S = r1 - r0
+            taps = {}
+            for site, buf in got.items():
+                if site.endswith(".softmax"):
+                    n = m.num_heads * S * S
+                    taps[site] = buf[sq:sq + n].reshape(m.num_heads, S, S).copy()
+                else:
+                    w = m.intermediate if site.endswith(".ffn.mid") else m.hidden
+                    taps[site] = buf.reshape(-1, w)[r0:r1].copy()
+            sq += m.num_heads * S * S
+            out.append((res.hidden_states[r0:r1].copy(), taps))
+        return out
+
     # ------------------------------------------------------------ analyze-quant
     def code_usage(self, encs, plan: PrecisionPlan) -> dict:
         """{site: CodeUsageReport} summed over ``encs`` for every site ``plan`` quantizes:
         one device forward with histogram taps on the INT8 codes the kernels write (the
         reference's tap -> quantize -> code_usage loop, cli.py:284-292)."""
-        self.check_plan(plan)
         for e in encs:
             self._validate(e, self.manifest)
-        self._push_calibration()
         seq_start, att, ids, segs = self.pack(encs)
         sites = activation_sites(self.manifest.num_layers)
         counts = np.zeros((len(sites), 256), np.uint64)
         with self._lock:
+            self.check_plan(plan)
+            self._push_calibration()
             _lib.check(self._lib.samp_code_usage(self._h, plan.codes(), len(encs), seq_start.ctypes.data,
                                                  att.ctypes.data, ids.ctypes.data, segs.ctypes.data,
                                                  counts.ctypes.data))
@@ -325,8 +377,9 @@ class Engine:
         return {s: usage[s] for s in selected}
 
     # ------------------------------------------------------------ debug / parity
-    def set_capture(self, on: bool) -> None:
-        _lib.check(self._lib.samp_set_capture(self._h, int(bool(on))))
+    def set_capture(self, on) -> None:
+        """0 off, 1 (True) stage buffers for teacher-forced checks, 2 stages + F32 site taps."""
+        _lib.check(self._lib.samp_set_capture(self._h, int(on)))
 
     def fetch_stage(self, name: str, layer: int, dtype, shape) -> np.ndarray:
         size = ctypes.c_size_t()

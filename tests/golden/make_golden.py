@@ -122,8 +122,9 @@ def main():
     calib = random_inputs(500, [(64, 64), (64, 50), (64, 33), (64, 64)], seed=11)
     inputs = random_inputs(500, [(64, 64), (64, 40), (64, 17)], seed=12)
     plans = [("FP", 0), ("FULLY_QUANT", 1), ("FULLY_QUANT", 2), ("FFN_ONLY", 2)]
+    # fp16 storage (reference --mode fp16, Engine(fp16_storage=True), encoder.py:428) too
     dump_case("mini", recipe, "classification", plans, inputs, calib_inputs=calib,
-              taps_plan=("FULLY_QUANT", 2))
+              fp16_modes=(False, True), taps_plan=("FULLY_QUANT", 2))
 
     # 3. one BERT-base-shaped layer (H=768, 12 heads, I=3072) at S=128: pins the
     #    768-wide LN tree and the 128-key softmax tree at the real sizes
@@ -132,9 +133,9 @@ def main():
                   weight_scale=0.02, vocab_extra=extra)
     calib = random_inputs(1000, [(128, 128), (128, 100)], seed=21)
     inputs = random_inputs(1000, [(128, 128), (128, 77)], seed=22)
-    plans = [("FULLY_QUANT", 1), ("FFN_ONLY", 1)]
+    plans = [("FULLY_QUANT", 1), ("FFN_ONLY", 1), ("FP", 0)]
     dump_case("base1", recipe, "sequence_labeling", plans, inputs, calib_inputs=calib,
-              taps_plan=("FULLY_QUANT", 1))
+              fp16_modes=(False, True), taps_plan=("FULLY_QUANT", 1))
 
 
 def analyze_golden():

@@ -44,9 +44,10 @@ class Workload:
     (configs[1]); c4 / c5 are the other throughput configs, selectable with --workload
     (their scales come from on-device calibration, 8 rng(1) sequences)."""
 
-    def __init__(self, key, desc, model, task, labels, batch, seq, mode, pairs=False, strong=False):
+    def __init__(self, key, desc, model, task, labels, batch, seq, mode, pairs=False, strong=False, varlen=None):
         self.key, self.desc, self.model, self.task, self.labels = key, desc, model, task, labels
         self.batch, self.seq, self.mode, self.pairs, self.strong = batch, seq, mode, pairs, strong
+        self.varlen = varlen      # (lo, hi): sequence lengths rng(0).integers(lo, hi + 1)
 
 
 WORKLOADS = {
@@ -54,6 +55,9 @@ WORKLOADS = {
                    "bert-base", "classification", 2, 32, 128, "FULLY_QUANT"),
     "c4": Workload("c4", "BERT-large NER tag head, MHA-FFN INT8 24/24, batch 64 x seq 256 sharded over the GPUs "
                    "(configs[3])", "bert-large", "sequence_labeling", 9, 64, 256, "FULLY_QUANT", strong=True),
+    "c3": Workload("c3", "BERT-base self-adaptive sweep on a variable-length batch, S in [16, 512] (rng(0)), 64 "
+                   "sequences per GPU, token-balanced shards (configs[2]); value = FULLY_QUANT 12/12", "bert-base",
+                   "classification", 2, 64, 512, "FULLY_QUANT", varlen=(16, 512)),
     "c5": Workload("c5", "BERT-base text-matching pairs, FFN-only INT8 12/12, batch 4096 x seq 64 sharded over "
                    "the GPUs (configs[4])", "bert-base", "text_matching", 2, 4096, 64, "FFN_ONLY",
                    pairs=True, strong=True),
@@ -77,7 +81,7 @@ def build_model(wl=None):
 
     wl = wl or WORKLOADS["c2"]
     arch = bert_archive(wl.model, task=wl.task, num_labels=wl.labels, seed=0, weight_scale=0.02)
-    if wl.key != "c2":
+    if wl.model != MODEL or wl.task != "classification":
         return arch          # calibrated on the device by the caller
     with open(CALIB) as fh:
         table = CalibrationTable.from_json(fh.read())
@@ -85,6 +89,26 @@ def build_model(wl=None):
         raise RuntimeError("bench calibration does not belong to the bench archive (fingerprint mismatch)")
     arch.calibration = table
     return arch
+
+
+def workload_batch(wl, rank: int, world: int):
+    """This rank's packed batch: fixed-length workloads as synthetic_batch (weak: own batch
+    per rank; strong: 1/world of it), varlen (c3): the global batch of batch*world sequences
+    with rng(0) lengths and ids, cut into token-balanced contiguous shards
+    (sharding.partition_by_tokens)."""
+    if wl.varlen is None:
+        n = wl.batch // world if wl.strong else wl.batch
+        return synthetic_batch(rank, n, wl.seq, wl.pairs)
+    from paper_2209_09130_b200.sharding import partition_by_tokens
+    rng = np.random.default_rng(0)
+    lens = rng.integers(wl.varlen[0], wl.varlen[1] + 1, size=wl.batch * world)
+    ids_all = rng.integers(0, 30522, size=int(lens.sum())).astype(np.int32)
+    s0, s1 = partition_by_tokens(lens, world)[rank]
+    start_all = np.concatenate([[0], np.cumsum(lens)])
+    mine = lens[s0:s1]
+    seq_start = np.concatenate([[0], np.cumsum(mine)]).astype(np.int32)
+    ids = ids_all[start_all[s0]:start_all[s1]]
+    return seq_start, mine.astype(np.int32), ids, np.zeros_like(ids)
 
 
 def synthetic_batch(rank: int, batch: int = BATCH, seq: int = SEQ, pairs: bool = False):
@@ -164,6 +188,74 @@ def gemm_ops(T: int, H: int, I: int) -> dict:
             "ffn1_f16": 2 * T * H * I, "ffn2_f16": 2 * T * I * H}
 
 
+def run_sweep(eng, lib, wl, L, nseq, seq_start, att, d_ids, d_segs, head_kind, timed_steps, dev):
+    import torch
+    from paper_2209_09130_b200 import _lib
+    from paper_2209_09130_b200.allocator import (InfeasibleError, Profile, ProfilePoint, allocate_decay_aware,
+                                                 rank_by_ratio, select_by_accuracy_threshold,
+                                                 select_by_latency_threshold)
+    from paper_2209_09130_b200.engine import IO_DEVICE
+    from paper_2209_09130_b200.plan import FFN_ONLY, FULLY_QUANT, MHA_ONLY, PrecisionPlan
+    nl = eng.manifest.num_labels
+    lg = torch.empty((nseq, nl), dtype=torch.float32, device=dev)
+    pr, lab = torch.empty_like(lg), torch.empty(nseq, dtype=torch.int32, device=dev)
+    out = _lib.Outputs(None, lg.data_ptr(), pr.data_ptr(), lab.data_ptr(), head_kind)
+
+    def point(mode, k):
+        codes = PrecisionPlan.prefix(mode, L, k).codes()
+
+        def fwd():
+            st = torch.cuda.current_stream(dev).cuda_stream
+            _lib.check(lib.samp_forward(eng.handle, codes, nseq, seq_start.ctypes.data, att.ctypes.data,
+                                        d_ids.data_ptr(), d_segs.data_ptr(), IO_DEVICE, out, st))
+        for _ in range(3):
+            fwd()
+        ms = timed_steps(5, fwd) / 5
+        return ms, lab.cpu().numpy().copy()
+
+    base_ms, base_lab = point("FP", 0)
+    res = {"target": {"accuracy": "label agreement with the all-FP plan > 0.99",
+                      "latency": "below the midpoint of the FP and the all-INT8 (FULLY_QUANT 12) latency"},
+           "unit": "ms per forward of this batch (device, L2 flushed)", "modes": {}}
+    allq = None
+    profiles = {}
+    for mode in (FULLY_QUANT, FFN_ONLY, MHA_ONLY):
+        pts = [ProfilePoint(0, 1.0, base_ms * 1e-3, 1.0)]
+        for k in range(2, L + 1, 2):
+            ms, labs = point(mode, k)
+            pts.append(ProfilePoint(k, float(np.mean(labs == base_lab)), ms * 1e-3, base_ms / ms))
+        profiles[mode] = Profile(mode, pts)
+        if mode == FULLY_QUANT:
+            allq = pts[-1].latency
+    budget = 0.5 * (base_ms * 1e-3 + allq)
+    for mode, prof in profiles.items():
+        def pick(fn):
+            try:
+                return prof.points[fn()].quantized_layers
+            except InfeasibleError:
+                return None
+        res["modes"][mode] = {
+            "points": [{"k": p.quantized_layers, "ms": round(p.latency * 1e3, 4), "speedup": round(p.speedup, 3),
+                        "agreement": round(p.accuracy, 4)} for p in prof.points],
+            "decay_aware_k": pick(lambda: allocate_decay_aware(prof)),
+            "accuracy_target_k": pick(lambda: select_by_accuracy_threshold(prof, 0.99)),
+            "latency_target_k": pick(lambda: select_by_latency_threshold(prof, budget)),
+            "ratio_top5_k": [prof.points[i].quantized_layers for i in rank_by_ratio(prof, 5)]}
+    return res
+
+
+def max_over_ranks_int(x: int, world: int, dev, backend) -> list:
+    """every rank's x (all-gather of one int)"""
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [int(v.item()) for v in out]
+
+
 def run_samp(args):
     import torch
     import torch.distributed as dist
@@ -188,7 +280,6 @@ def run_samp(args):
     from paper_2209_09130_b200.plan import PrecisionPlan
 
     wl = WORKLOADS[args.workload]
-    BATCH, SEQ = (wl.batch // world if wl.strong else wl.batch), wl.seq
     if wl.strong and wl.batch % world:
         raise SystemExit(f"--workload {wl.key}: batch {wl.batch} does not split over {world} GPUs")
     arch = build_model(wl)
@@ -196,15 +287,18 @@ def run_samp(args):
     L = arch.manifest.num_layers
     if arch.calibration is None:
         from paper_2209_09130_b200.tokenization import EncodedInput
-        c_start, _, c_ids, c_segs = synthetic_batch(1, 8, SEQ, wl.pairs)
+        c_start, _, c_ids, c_segs = synthetic_batch(1, 8, wl.seq, wl.pairs)
         arch.calibration = eng.calibrate([EncodedInput(c_ids[c_start[i]:c_start[i + 1]].tolist(),
-                                                       c_segs[c_start[i]:c_start[i + 1]].tolist(), SEQ)
+                                                       c_segs[c_start[i]:c_start[i + 1]].tolist(), wl.seq)
                                           for i in range(8)])
         eng._push_calibration()
     plan = PrecisionPlan.prefix(wl.mode, L, L)
     head_kind = HEAD_TAG if wl.task == "sequence_labeling" else HEAD_CLASSIFY
-    seq_start, att, ids, segs = synthetic_batch(rank, BATCH, SEQ, wl.pairs)
+    seq_start, att, ids, segs = workload_batch(wl, rank, world)
+    BATCH, SEQ = len(att), wl.seq            # sequences on this rank; (max) tokens per sequence
+    lens = np.diff(seq_start).astype(np.int64)
     T = int(seq_start[-1])
+    total_seqs = int(sum(max_over_ranks_int(BATCH, world, dev, backend)))
     d_ids = torch.from_numpy(ids).to(dev)
     d_segs = torch.from_numpy(segs).to(dev)
     nl = arch.manifest.num_labels
@@ -265,7 +359,7 @@ def run_samp(args):
     ms = timed_steps(args.steps, fwd)
     barrier()
     job_ms = max_over_ranks(ms)
-    value = world * BATCH * args.steps / (job_ms / 1e3)
+    value = total_seqs * args.steps / (job_ms / 1e3)
 
     # ---------------- e2e through the public API with host buffers
     barrier()
@@ -280,13 +374,13 @@ def run_samp(args):
             e2e_ms += (t1 - t0) * 1e3
         assert res.labels is not None
     e2e_ms = max_over_ranks(e2e_ms)
-    e2e = {"value": world * BATCH * args.steps / (e2e_ms / 1e3), "unit": "sentences/s",
+    e2e = {"value": total_seqs * args.steps / (e2e_ms / 1e3), "unit": "sentences/s",
            "h2d_bytes_per_step": int(ids.nbytes + segs.nbytes),
            "d2h_bytes_per_step": int(rows * nl * 4 * 2 + rows * 4)}
 
     # ---------------- raw text end to end: native tokenizer + forward (extra information)
     e2e_text = None
-    if not wl.pairs:
+    if not wl.pairs and wl.varlen is None:
         from paper_2209_09130_b200.tokenization import Vocab, encode_batch
         v = arch.vocab
         vs = Vocab(v.token_to_id, do_lower_case=v.do_lower_case, max_seq_len=SEQ)
@@ -304,7 +398,7 @@ def run_samp(args):
             if i >= args.warmup:
                 t_tot += time.perf_counter() - t0
         t_tot = max_over_ranks(t_tot)
-        e2e_text = {"value": round(world * BATCH * args.steps / t_tot, 1), "unit": "sentences/s",
+        e2e_text = {"value": round(total_seqs * args.steps / t_tot, 1), "unit": "sentences/s",
                     "input": f"{BATCH} raw texts of {SEQ - 2} vocabulary words per GPU per step",
                     "tokenizer": "native multi-threaded (samp_tokenize_batch)"}
 
@@ -317,13 +411,13 @@ def run_samp(args):
     prof = json.loads(buf.value.decode())
     H, I = arch.manifest.hidden, arch.manifest.intermediate
     ops = gemm_ops(T, H, I)
-    ops["attention_i8"] = 4 * BATCH * SEQ * SEQ * H
-    ops["attention_f16"] = 4 * BATCH * SEQ * SEQ * H
+    ops["attention_i8"] = 4 * int((lens ** 2).sum()) * H
+    ops["attention_f16"] = 4 * int((lens ** 2).sum()) * H
     # HBM-bound kernels: algorithmic bytes per launch (DESIGN.md kernel table): the embed
     # reads each token's F32 word row and writes its row (int8 on INT8 plans), plus ids /
     # segments / positions; position / type rows and gamma / beta are read once
     out_bytes = 1 if wl.mode == "FULLY_QUANT" else 6     # int8, or f32 + f16 rows
-    hbm_bytes = {"embed": T * (4 * H + out_bytes * H + 12) + SEQ * 4 * H + 2 * 4 * H + 2 * 4 * H}
+    hbm_bytes = {"embed": T * (4 * H + out_bytes * H + 12) + int(lens.max()) * 4 * H + 2 * 4 * H + 2 * 4 * H}
     hbm_peak = (json.load(open(PEAKS)).get("hbm_gbs") if os.path.exists(PEAKS) else None) or 6650.0
     kernels = {}
     for name, (tot_ms, n) in prof.items():
@@ -357,10 +451,19 @@ def run_samp(args):
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "ops_per_launch": ops[dom]}
 
+    # ---------------- self-adaptive sweep (configs[2]; reference allocator.build_profile,
+    # allocator.py:265-306): every prefix plan k = 0, 2, ..., L of each mode on this batch,
+    # device time per forward and label agreement with the all-FP plan (random weights: no
+    # task accuracy exists, agreement with the FP model is the accuracy proxy), then the
+    # allocator's picks on those profiles
+    sweep = None
+    if wl.model == MODEL and wl.task == "classification":
+        sweep = run_sweep(eng, lib, wl, L, BATCH, seq_start, att, d_ids, d_segs, head_kind, timed_steps, dev)
+
     # ---------------- batch-1 p50 latency per mode (device time, L2 flushed)
     clocks.__exit__(None, None, None)
     lat = {}
-    b1_start, b1_att = np.array([0, SEQ], np.int32), np.array([SEQ], np.int32)
+    b1_start, b1_att = np.array([0, 128], np.int32), np.array([128], np.int32)   # metric: seq 128
     out1 = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), head_kind)
     for label, mode, k in (("fp16", "FP", 0), (f"ffn-only-{L}", "FFN_ONLY", L), (f"fully-quant-{L}", "FULLY_QUANT", L)):
         pc = PrecisionPlan.prefix(mode, L, k).codes()
@@ -393,13 +496,17 @@ def run_samp(args):
             "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic (random ids, random-init weights seed 0; reference-calibrated scales)",
             "config": {"workload": wl.desc, "encoder": wl.model, "plan": f"{wl.mode} k={L}",
-                       "sequences_per_gpu": BATCH, "tokens_per_sequence": SEQ, "sequences_total": BATCH * world,
+                       "sequences_per_gpu": BATCH, "tokens_per_gpu": T,
+                       "tokens_per_sequence": SEQ if wl.varlen is None else f"{int(lens.min())}..{int(lens.max())}",
+                       "sequences_total": total_seqs,
                        "sharding": f"independent replicas x{world} (sequences partitioned, no collective)",
                        "l2": "flushed before every timed step (256 MiB write)",
-                       "calibration": "reference (tests/golden)" if wl.key == "c2" else "on-device, 8 rng(1) sequences"},
+                       "calibration": "reference (tests/golden)" if wl.model == MODEL and wl.task == "classification"
+                       else "on-device, 8 rng(1) sequences"},
             "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
             "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps, "e2e_text": e2e_text,
             "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels, "parity": parity,
+            "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -134,7 +134,12 @@ int samp_sync(samp_engine* e);
 
 /* Debug/parity: after samp_forward with samp_set_capture(e, 1), copy the named
  * stage buffer of `layer` (names in DESIGN.md: in_q, qkv_q, ctx_q, ffn_in_q, mid_q,
- * out_q, out_f32, embed_f32, ...) to host; *bytes receives the size. */
+ * out_q, out_f32, embed_f32, ...) to host; *bytes receives the size.
+ * samp_set_capture(e, 2) also records Engine.run(..., capture_taps=True)'s taps
+ * (reference encoder.py:238-240 _tap; sites :294-311, :324-327, :360-379, :407-417):
+ * stage "tap:<site>" at layer -1 holds the site's F32 values for the packed batch,
+ * [T][H] ([T][I] for L.ffn.mid), and L.attn.softmax as each sequence's [heads][S][S]
+ * in batch order.  INT8-chain sites are bit-exact with the reference. */
 int samp_set_capture(samp_engine* e, int on);
 int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, size_t capacity, size_t* bytes);
 
@@ -142,6 +147,9 @@ int samp_fetch_stage(samp_engine* e, const char* name, int layer, void* dst, siz
  * B is given in the reference layout [k][n] row-major (activation @ weight). */
 int samp_debug_gemm_i8(const int8_t* a, const int8_t* b, int32_t* c, int m, int n, int k);
 int samp_debug_gemm_f16(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);
+/* main-loop ceiling of the repo's tcgen05 GEMM (plain accumulator store, device-resident
+ * operands): kind 0 = kind::i8, 1 = kind::f16; *ms = average of `iters` launches */
+int samp_debug_gemm_peak(int kind, int m, int n, int k, int iters, float* ms);
 
 /* Native multi-threaded host tokenizer (the paper's C++ tokenizer feeding the packed
  * varlen batch; replaces the reference's per-text tokenization.encode loop, cli.py:375-377,

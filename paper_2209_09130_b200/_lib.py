@@ -71,6 +71,8 @@ SIGNATURES = [
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("samp_debug_gemm_f16", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("samp_debug_gemm_peak", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
     ("samp_debug_quant_exhaustive", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_div_exhaustive", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("samp_debug_exp_exhaustive", ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),

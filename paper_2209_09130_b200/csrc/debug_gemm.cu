@@ -85,3 +85,52 @@ extern "C" int samp_debug_gemm_i8(const int8_t* a, const int8_t* b, int32_t* c, 
 extern "C" int samp_debug_gemm_f16(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k) {
   return samp::guarded([&] { samp::debug_gemm<samp::KIND_F16>(a, b, c, m, n, k); });
 }
+
+// Tensor-pipe ceiling of this GEMM's main loop: an m x n x k product with the plain
+// accumulator-store epilogue (BN = 256, 4-stage ring, one 128-row tile per CTA) on
+// device-resident operands, `iters` launches back to back; *ms = average per launch.
+// (tools/peak_gemm.py reports it next to the library INT8 / FP16 peaks.)
+extern "C" int samp_debug_gemm_peak(int kind, int m, int n, int k, int iters, float* ms) {
+  return samp::guarded([&] {
+    using namespace samp;
+    const int eb = kind == KIND_I8 ? 1 : 2;
+    SAMP_REQUIRE(m % 128 == 0 && n % 256 == 0 && (k * eb) % 128 == 0 && iters >= 1, SAMP_E_DIMENSION,
+                 "peak gemm needs m % 128, n % 256, k*elt % 128 == 0");
+    void *da, *db, *dc;
+    SAMP_CUDA(cudaMalloc(&da, size_t(m) * k * eb));
+    SAMP_CUDA(cudaMalloc(&db, size_t(n) * k * eb));
+    SAMP_CUDA(cudaMalloc(&dc, size_t(m) * n * 4));
+    SAMP_CUDA(cudaMemset(da, 0x11, size_t(m) * k * eb));
+    SAMP_CUDA(cudaMemset(db, 0x22, size_t(n) * k * eb));
+    CUtensorMap ma, mb;
+    if (kind == KIND_I8) {
+      ma = tmap_i8(da, m, k, k, 128, 128);
+      mb = tmap_i8(db, n, k, k, 128, 256);
+    } else {
+      ma = tmap_f16(da, m, k, k, 64, 128);
+      mb = tmap_f16(db, n, k, k, 64, 256);
+    }
+    EpiStoreAcc::Params p{dc, n};
+    auto launch = [&]() {
+      return kind == KIND_I8 ? launch_gemm<KIND_I8, 256, 4, 1, 4, EpiStoreAcc>(ma, mb, m, n, k * eb, p, 0)
+                             : launch_gemm<KIND_F16, 256, 4, 1, 4, EpiStoreAcc>(ma, mb, m, n, k * eb, p, 0);
+    };
+    SAMP_CUDA(launch());
+    SAMP_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, 0);
+    for (int i = 0; i < iters; ++i) SAMP_CUDA(launch());
+    cudaEventRecord(b, 0);
+    SAMP_CUDA(cudaEventSynchronize(b));
+    float t = 0;
+    cudaEventElapsedTime(&t, a, b);
+    *ms = t / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dc);
+  });
+}

@@ -231,7 +231,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
       const uint32_t pa = smem_addr(smem + lay.p_off), va = smem_addr(smem + lay.v_off);
       const uint32_t idesc2 = F16 ? idesc_f16(128, 64, true) : idesc_i8(128, 64, true);
       for (int ch = 0; ch < nchunks; ++ch) {
-        mbar_wait(bar_p, ch & 1);
+        mbar_wait_sleep(bar_p, ch & 1);   // the softmax passes take microseconds
         tc_fence_after();
         const int k_lo = ch * ATT_P_CHUNK, k_hi = min(nkp, k_lo + ATT_P_CHUNK);
         for (int key = k_lo; key < k_hi; key += C::KEY_STEP) {
@@ -263,7 +263,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     const bool live = cnt > 1 ? r < nk : q0 + r < S;
     const int nrow = (S + 31) & ~31;                   // this row's key chunks: [kbeg, kbeg + nrow)
     const float m = p.mult_scores;
-    mbar_wait(bar_s, 0);
+    mbar_wait_sleep(bar_s, 0);            // Q/K/V loads + MMA 1 (after the PDL wait)
     tc_fence_after();
     const bool stamper = stamp && threadIdx.x == 32;
     if (stamper) stamp[2] = globaltimer();
@@ -338,7 +338,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
           v[j + 1] = __float_as_uint(clean || c0 + j + 1 < att ? e.y : 0.0f);
         }
       } else {
-#pragma unroll 4
+        // fully unrolled: a runtime index would put v[] in local memory for both paths
+#pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int key = c0 + j;
           float x = xval(as_acc(v[j]));
@@ -416,7 +417,9 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
               w[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
             }
           } else {
-            // probabilities are >= +0, so quantize's copysign(0.5, y) is +0.5
+            // probabilities are >= +0, so quantize's copysign(0.5, y) is +0.5.  Keys past S
+            // hold e = +0 (pass 2), so their P = +0 / sum = +0 and t = 0.5 truncates to code
+            // 0: no per-key select is needed
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               float2 q[2];
@@ -425,8 +428,6 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
                 const float2 pv = div_pair(f2(__uint_as_float(v[j + 2 * u]), __uint_as_float(v[j + 2 * u + 1])),
                                            rden_r, rden_ns);
                 q[u] = add2(div_pair(pv, rsm_r, rsm_ns), f2(0.5f, 0.5f), kx);
-                q[u].x = key0 + j + 2 * u < S ? q[u].x : 0.0f;
-                q[u].y = key0 + j + 2 * u + 1 < S ? q[u].y : 0.0f;
               }
               w[j / 4] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
               if (hist_s && live) {   // code-usage tap over the row's S keys (masked ones included)
@@ -452,7 +453,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     if (stamper) stamp[6] = globaltimer();
     // context rows: h writes output columns [OC*h, OC*h + OC), OC = 64 / TPR
     constexpr int OC = 64 / TPR;
-    mbar_wait(bar_pf, (nchunks - 1) & 1);
+    mbar_wait_sleep(bar_pf, (nchunks - 1) & 1);
     tc_fence_after();
     uint32_t o[OC];
     if constexpr (OC == 32) tmem_ld32(ta + OC * h, o);

@@ -67,6 +67,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// one try_wait (returns whether the phase with `parity` has completed)
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+// Long waits (microseconds: a warp waiting for another role's whole phase) back off with
+// __nanosleep so the spinning warp does not take issue slots from the warps doing the
+// work on its SM sub-partition (ncu: 8.5% of the attention kernel's instructions were the
+// MMA warp's try_wait loop).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 64;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 512 ? 2 * ns : 512;
+  }
+}
+
 // ------------------------------------------------------------------ PDL
 // Programmatic dependent launch.  Every kernel is launched with programmatic stream
 // serialization, so it may start while its predecessor is still running:

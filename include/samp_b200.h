@@ -125,6 +125,13 @@ int samp_code_usage(samp_engine* e, const uint8_t* layer_prec, int32_t nseq, con
                     const int32_t* att_len, const int32_t* ids, const int32_t* segs,
                     unsigned long long* counts);
 
+/* Exact FP32 layers (Engine(exact_fp32=True)): the FP blocks (mha_fp / ffn_fp,
+ * encoder.py:276-330 — FP plans, FFN_ONLY's attention, MHA-only's FFN) run the reference's
+ * k-ordered FP32 GEMMs (kernels.py:48-71, 188-200) on the FP32 pipe instead of the FP16
+ * tensor cores, so every plan's hidden states are bit-exact with the reference (and
+ * Engine.calibrate equals its FP32 calibration).  Off by default (FP16 tensor cores). */
+int samp_set_exact_fp32(samp_engine* e, int on);
+
 /* CUDA-graph replay of the forward per (plan, batch geometry, head): on by default;
  * a key is captured on its second use and replayed afterwards */
 int samp_set_graphs(samp_engine* e, int on);

@@ -62,6 +62,7 @@ SIGNATURES = [
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     ("samp_code_usage", ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int32, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("samp_set_exact_fp32", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("samp_set_graphs", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("samp_sync", ctypes.c_int, [ctypes.c_void_p]),
     ("samp_set_capture", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

@@ -64,6 +64,7 @@ struct LayerDev {
   int8_t *qkv_i8 = nullptr, *wo_i8 = nullptr, *w1_i8 = nullptr, *w2_i8 = nullptr;    // K-major
   __half *qkv_f16 = nullptr, *wo_f16 = nullptr, *w1_f16 = nullptr, *w2_f16 = nullptr;
   float *qkv_b = nullptr, *ob = nullptr, *ln1_g = nullptr, *ln1_b = nullptr;
+  float *qkv32 = nullptr, *wo32 = nullptr, *w132 = nullptr, *w232 = nullptr;   // exact FP32: (in, out)
   float *b1 = nullptr, *b2 = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
   double s_w[6] = {0, 0, 0, 0, 0, 0};  // qw kw vw ow w1 w2
   double b1_absmax = 0;                 // max|b1|: bounds the FFN1 GELU argument
@@ -191,6 +192,10 @@ struct samp_engine {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   std::map<std::string, std::pair<double, long>> prof;  // name -> (total ms, launches)
+  // exact FP32 layers (samp_set_exact_fp32): FP blocks on the k-ordered FP32 SIMT path
+  bool exact = false;
+  int exact_cap = 0;
+  float *x_qkv = nullptr, *x_ctx = nullptr, *x_proj = nullptr, *x_mid = nullptr;
   // capture_taps (samp_set_capture(e, 2)): F32 site values, recorded as stages "tap:<site>"
   bool taps = false;
   int tap_cap = 0;                 // token rows of the tap scratch buffers
@@ -415,6 +420,19 @@ static void ensure_taps(samp_engine* e) {
   SAMP_CUDA(cudaMemcpy(e->tap_prob_off, off.data(), g.nseq * sizeof(long long), cudaMemcpyHostToDevice));
 }
 
+static void ensure_exact(samp_engine* e) {
+  const int T = e->geo.T, H = e->d.hidden, I = e->d.intermediate;
+  if (T <= e->exact_cap) return;
+  clear_graphs(e);
+  for (void* q : {(void*)e->x_qkv, (void*)e->x_ctx, (void*)e->x_proj, (void*)e->x_mid})
+    if (q) e->mem.release(q);
+  e->exact_cap = std::max(T, 128);
+  e->x_qkv = e->mem.alloc<float>(size_t(e->exact_cap) * 3 * H);
+  e->x_ctx = e->mem.alloc<float>(size_t(e->exact_cap) * H);
+  e->x_proj = e->mem.alloc<float>(size_t(e->exact_cap) * H);
+  e->x_mid = e->mem.alloc<float>(size_t(e->exact_cap) * I);
+}
+
 static cudaEvent_t take_event(samp_engine* e) {
   if (e->event_pool.empty()) {
     cudaEvent_t ev;
@@ -586,6 +604,71 @@ static void taps_ffn_mid(samp_engine* e, int i, bool f16, const CUtensorMap& a_m
   tap_record(e, lsite(i, "ffn", "mid"), e->tap_out, size_t(T) * I * 4);
 }
 
+// capture_taps of q/k/v out of an interleaved [T][3H] f32 buffer
+static void tap_qkv_f32(samp_engine* e, int i, const float* qkv) {
+  if (!e->taps) return;
+  const int T = e->geo.T, H = e->d.hidden;
+  const char* nm[3] = {"q", "k", "v"};
+  for (int k = 0; k < 3; ++k) {
+    SAMP_CUDA(cudaMemcpy2DAsync(e->tap_out, size_t(H) * 4, qkv + size_t(k) * H, size_t(3) * H * 4, size_t(H) * 4, T,
+                                cudaMemcpyDeviceToDevice, e->stream_in_use));
+    tap_record(e, lsite(i, "attn", nm[k]), e->tap_out, size_t(T) * H * 4);
+  }
+}
+
+// Exact FP32 MHA block (reference mha_fp, encoder.py:276-312): hid_f32 -> ln1_f32 (and the
+// ffn.in codes when the FFN runs INT8).  rnd: fp16-storage rounding of this block's stored
+// values (FP layers only; FFN_ONLY's MHA runs unrounded, encoder.py:495-497).
+static void exact_mha(samp_engine* e, int i, const LayerDev& w, int rnd, bool int8_ffn) {
+  const int T = e->geo.T, H = e->d.hidden;
+  const Geometry& g = e->geo;
+  Activations& a = e->act;
+  cudaStream_t st = e->stream_in_use;
+  float* cal = e->calib_amax;
+  const int cbase = 1 + 8 * i;
+  ExactGemmParams q{a.hid_f32, H, w.qkv32, 3 * H, T, 3 * H, H, w.qkv_b, 0, rnd, e->x_qkv, 3 * H, cal, cbase + 1, H};
+  check_launch(e, launch_exact_gemm(q, e->sms, st), "qkv_f32");
+  tap_qkv_f32(e, i, e->x_qkv);
+  ExactAttnParams ap{e->x_qkv, H, g.d_seq_start, g.d_att_len, f32(1.0 / std::sqrt(double(H / e->d.num_heads))), rnd,
+                     e->x_ctx, e->taps ? e->tap_probs : nullptr, e->tap_prob_off, cal, cbase + 4, cbase + 5};
+  check_launch(e, launch_exact_attention(ap, g.max_s, e->d.num_heads, g.nseq, st), "attention_f32");
+  tap_record(e, lsite(i, "attn", "softmax"), e->tap_probs, e->tap_probs_total * 4);
+  tap_record(e, lsite(i, "attn", "out_in"), e->x_ctx, size_t(T) * H * 4);
+  ExactGemmParams o{e->x_ctx, H, w.wo32, H, T, H, H, nullptr, 0, 0, e->x_proj, H, nullptr, 0, 0};
+  check_launch(e, launch_exact_gemm(o, e->sms, st), "outproj_f32");
+  ExactLnParams ln{e->x_proj, w.ob, a.hid_f32, w.ln1_g, w.ln1_b, f32(e->d.layernorm_eps), T, rnd, a.ln1_f32,
+                   nullptr, 0.0f, cal, cbase + 6};
+  if (int8_ffn) {   // x_q = quantize(mha_out, ffn.in) (encoder.py:497-499)
+    ln.out_i8 = a.ffn_in_i8;
+    ln.s_out = f32(sc(e, lsite(i, "ffn", "in")));
+  }
+  check_launch(e, launch_exact_ln(ln, H, st), "ln1_f32");
+  tap_record(e, lsite(i, "ffn", "in"), a.ln1_f32, size_t(T) * H * 4);
+}
+
+// Exact FP32 FFN block (reference ffn_fp, encoder.py:315-330) on ln1_f32 (FP layers: the MHA
+// output; MHA-only layers: dequantized ffn.in codes); the output is quantized for a next
+// INT8-attention layer or stays F32 in hid_f32.
+static void exact_ffn(samp_engine* e, int i, const LayerDev& w, int rnd, bool next_int8, int8_t* next_q) {
+  const int T = e->geo.T, H = e->d.hidden, I = e->d.intermediate, L = e->d.num_layers;
+  Activations& a = e->act;
+  cudaStream_t st = e->stream_in_use;
+  float* cal = e->calib_amax;
+  ExactGemmParams g1{a.ln1_f32, H, w.w132, I, T, I, H, w.b1, 1, rnd, e->x_mid, I, cal, 1 + 8 * i + 7, 0};
+  check_launch(e, launch_exact_gemm(g1, e->sms, st), "ffn1_f32");
+  tap_record(e, lsite(i, "ffn", "mid"), e->x_mid, size_t(T) * I * 4);
+  ExactGemmParams g2{e->x_mid, I, w.w232, H, T, H, I, nullptr, 0, 0, e->x_proj, H, nullptr, 0, 0};
+  check_launch(e, launch_exact_gemm(g2, e->sms, st), "ffn2_f32");
+  ExactLnParams ln{e->x_proj, w.b2, a.ln1_f32, w.ln2_g, w.ln2_b, f32(e->d.layernorm_eps), T, rnd, a.hid_f32,
+                   nullptr, 0.0f, i + 1 < L ? cal : nullptr, 1 + 8 * (i + 1)};
+  if (next_int8) {
+    ln.out_f32 = e->taps ? e->tap_ln : nullptr;   // attn.in tap of the next layer
+    ln.out_i8 = next_q;
+    ln.s_out = f32(sc(e, input_site(i + 1)));
+  }
+  check_launch(e, launch_exact_ln(ln, H, st), "ln2_f32");
+}
+
 // one encoder layer; `in_q` = index of xq holding this layer's input codes (INT8 inputs)
 static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   const int L = e->d.num_layers, H = e->d.hidden, I = e->d.intermediate, T = e->geo.T;
@@ -686,8 +769,16 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     // reference fp16 storage rounds the FP layers' stored values; FFN_ONLY's MHA runs
     // without it (encoder.py:493-497 passes round_fn None)
     const int rnd = p == SAMP_LAYER_FP ? fp16_store : 0;
+    if (e->exact) {
+      exact_mha(e, i, w, rnd, p == SAMP_LAYER_FFN_INT8);
+      if (p == SAMP_LAYER_FFN_INT8) {
+        record(e, "ffn_in_q", i, a.ffn_in_i8, size_t(T) * H);
+        usage_tap(e, 1 + 8 * i + 6, a.ffn_in_i8, T, H, H);
+      }
+    }
     float* cal = e->calib_amax;
     const int cbase = 1 + 8 * i;   // activation_sites order: attn.in q k v softmax out_in ffn.in ffn.mid
+    if (!e->exact) {
     EpiF16Out::Params qp{a.qkv_f16, 3 * H, w.qkv_b, 0, cal, cbase + 1, H};
     if (qkv_narrow)   // small batches: 64-wide tiles, 4x the CTAs of the 256-wide default
       check_launch(e, gemm_f16out(64, a.a_hid_f16, w.m_qkv_f16_64, T, 3 * H, 2 * H, qp, st), "qkv_f16");
@@ -738,6 +829,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     } else {
       record(e, "ln1_f32", i, a.ln1_f32, size_t(T) * H * 4);
     }
+    }   // !e->exact
   }
 
   // ---------------- feed-forward block; output goes to xq[cur^1] (codes) or hid_f32/f16
@@ -781,6 +873,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.mult = mult_of(s_mid, w.s_w[5]);
     if (!ln_gemm_splitk(e, "ffn2_i8", a.a_mid_i8, w.m_w2_i8_64, I, lp, st))
       check_launch(e, gemm_ln_i8(tln, a.a_mid_i8, ln_small ? w.m_w2_i8_s : w.m_w2_i8, T, H, I, lp, st, a.a_mid_i8_mc), "ffn2_i8");
+  } else if (e->exact) {
+    exact_ffn(e, i, w, p == SAMP_LAYER_FP ? fp16_store : 0, next_int8, a.xq[cur ^ 1]);
   } else {
     EpiF16Out::Params gp{a.mid_f16, I, w.b1, 1, e->calib_amax, 1 + 8 * i + 7, 0};
     const int k1 = ffn1_bn_index(T, I, e->sms, false);   // EpiF16Out walks 32-column chunks
@@ -962,6 +1056,17 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
       SAMP_CUDA(launch_pack_weight(tmp, K, N, f32(scale), oi8, of16, row_off, 0));
       SAMP_CUDA(cudaDeviceSynchronize());
     };
+    // exact FP32 copies in the archive's (in, out) layout; QKV concatenated along out
+    w.qkv32 = e->mem.alloc<float>(size_t(H) * 3 * H);
+    for (int k = 0; k < 3; ++k)
+      SAMP_CUDA(cudaMemcpy2D(w.qkv32 + size_t(k) * H, size_t(3) * H * 4, t[2 * k], size_t(H) * 4, size_t(H) * 4, H,
+                             cudaMemcpyHostToDevice));
+    w.wo32 = e->mem.alloc<float>(size_t(H) * H);
+    SAMP_CUDA(cudaMemcpy(w.wo32, t[6], size_t(H) * H * 4, cudaMemcpyHostToDevice));
+    w.w132 = e->mem.alloc<float>(size_t(H) * I);
+    SAMP_CUDA(cudaMemcpy(w.w132, t[10], size_t(H) * I * 4, cudaMemcpyHostToDevice));
+    w.w232 = e->mem.alloc<float>(size_t(I) * H);
+    SAMP_CUDA(cudaMemcpy(w.w232, t[12], size_t(I) * H * 4, cudaMemcpyHostToDevice));
     pack(t[0], H, H, w.s_w[0], w.qkv_i8, w.qkv_f16, 0);
     pack(t[2], H, H, w.s_w[1], w.qkv_i8, w.qkv_f16, H);
     pack(t[4], H, H, w.s_w[2], w.qkv_i8, w.qkv_f16, 2 * H);
@@ -1069,6 +1174,14 @@ extern "C" int samp_clear_calibration(samp_engine* e) {
 
 extern "C" int samp_debug_gelu_fast_check(float s, unsigned long long* counts) {
   return guarded([&] { SAMP_CUDA(gelu_fast_check(s, gelu_inv_s(s), counts, nullptr)); });
+}
+
+extern "C" int samp_set_exact_fp32(samp_engine* e, int on) {
+  std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
+  return guarded([&] {
+    clear_graphs(e);
+    e->exact = on != 0;
+  });
 }
 
 extern "C" int samp_set_graphs(samp_engine* e, int on) {
@@ -1313,6 +1426,7 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
     }
     gelu_fast_prepare(e, prec);
     if (e->taps) ensure_taps(e);
+    if (e->exact) ensure_exact(e);
     // ---------------- device work: replay a captured CUDA graph for this (plan, batch
     // geometry, head) when one exists; capture on the second sighting of a key (the first
     // run also configures every kernel's smem attributes outside of capture)

@@ -80,6 +80,49 @@ struct TapAttnParams {
   const long long* prob_off;
   float* ctx;             // [T][H]
 };
+// exact FP32 layers (exact_fp32.cu): the reference's FP blocks bit for bit
+struct ExactGemmParams {
+  const float* a;         // [M][lda]
+  int lda;
+  const float* b;         // [K][ldb]  (archive (in, out) layout)
+  int ldb, M, N, K;
+  const float* bias;      // [N] or null
+  int gelu, f16_round;
+  float* out;             // [M][ldo]
+  int ldo;
+  float* amax;            // calibration (null = off): site + column block
+  int site, block_cols;
+};
+struct ExactAttnParams {
+  const float* qkv;       // [T][3H] f32
+  int hidden;
+  const int* seq_start;
+  const int* att_len;
+  float mult_scores;      // F32(1/sqrt(d))
+  int f16_round;
+  float* ctx;             // [T][H]
+  float* probs;           // capture_taps: per sequence [heads][S][S] at prob_off[seq] (or null)
+  const long long* prob_off;
+  float* amax;
+  int site_sm, site_ctx;
+};
+struct ExactLnParams {
+  const float* acc;       // [M][H] projection (no bias)
+  const float* bias;
+  const float* res;       // [M][H] f32 residual
+  const float* gamma;
+  const float* beta;
+  float eps;
+  int M, f16_round;
+  float* out_f32;         // or null
+  int8_t* out_i8;         // or null: quantize(s_out) of the (rounded) output
+  float s_out;
+  float* amax;
+  int site;
+};
+cudaError_t launch_exact_gemm(const ExactGemmParams& p, int sms, cudaStream_t st);
+cudaError_t launch_exact_attention(const ExactAttnParams& p, int max_s, int heads, int nseq, cudaStream_t st);
+cudaError_t launch_exact_ln(const ExactLnParams& p, int hidden, cudaStream_t st);
 cudaError_t launch_tap_bias(const TapBiasParams& p, cudaStream_t st);
 cudaError_t launch_tap_attention(const TapAttnParams& p, int max_s, int heads, int nseq, cudaStream_t st);
 cudaError_t gemm_store_acc(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int kb,

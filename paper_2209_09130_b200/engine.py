@@ -76,7 +76,12 @@ class BatchOutput:
 class Engine:
     """Loaded model on one GPU; safe to share across threads (calls are serialised)."""
 
-    def __init__(self, archive: ModelArchive, fp16_storage: bool = False, device: int = 0):
+    def __init__(self, archive: ModelArchive, fp16_storage: bool = False, device: int = 0,
+                 exact_fp32: bool = False):
+        """``exact_fp32``: run the floating-point blocks (FP layers, FFN_ONLY's attention,
+        MHA-only's FFN) on the FP32 pipe with the reference's k-ordered GEMM accumulation, so
+        every plan is bit-exact with the reference (samp_set_exact_fp32); default: FP16
+        tensor cores within tolerance."""
         self.archive = archive
         self.manifest = m = archive.manifest
         self.vocab = archive.vocab
@@ -104,6 +109,9 @@ class Engine:
             _lib.check(lib.samp_load_layer(self._h, i, ptrs))
         head = [f32(k) if k in t else None for k in ("pooler.weight", "pooler.bias", "head.weight", "head.bias")]
         _lib.check(lib.samp_load_heads(self._h, *[a.ctypes.data if a is not None else None for a in head]))
+        self.exact_fp32 = bool(exact_fp32)
+        if self.exact_fp32:
+            _lib.check(lib.samp_set_exact_fp32(self._h, 1))
         self._pushed_calibration = None
         self._push_calibration()
 

@@ -66,6 +66,7 @@ METRIC = "BERT-base seq128 sentences/s (1/2/4/8 B200) & batch-1 p50 latency per 
 CALIB = os.path.join(ROOT, "tests", "golden", f"bench_calibration_{MODEL}.json")
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC = os.path.join(ROOT, "profiles", "dram_traffic.json")
+TENSOR_PEAKS = os.path.join(ROOT, "profiles", "peaks_int8_f16.json")
 
 
 def dist_env():
@@ -179,6 +180,13 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def step_ops(wl, lens, H, I, L) -> float:
+    """Algorithmic GEMM ops of one forward: 2*T*L*(4H^2 + 2HI) for
+    the projections + 4*L*H*sum(S^2) for attention (QK^T and PV)."""
+    T = int(np.sum(lens))
+    return 2.0 * T * L * (4 * H * H + 2 * H * I) + 4.0 * L * H * float(np.sum(np.asarray(lens, np.float64) ** 2))
 
 
 def gemm_ops(T: int, H: int, I: int) -> dict:
@@ -434,22 +442,34 @@ def run_samp(args):
     for name, (tot_ms, _) in prof.items():
         kernels[name]["share"] = round(tot_ms / total, 4)
     dom = max((k for k in prof if k in ops), key=lambda k: prof[k][0])
+    # denominators: the measured dense peak of the matching kind, burst figure (each launch
+    # is timed on its own here): INT8 = cuBLASLt int8 GEMM, FP16 = cuBLAS f16 GEMM, both
+    # 8192^3 on this pool's B200 (tools/peak_gemm.py -> profiles/peaks_int8_f16.json)
+    tp = json.load(open(TENSOR_PEAKS)) if os.path.exists(TENSOR_PEAKS) else {}
+    i8_peak = (tp.get("int8_cublaslt") or {}).get("burst_tops")
+    f16_peak = (tp.get("f16_cublas") or {}).get("burst_tops")
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
-    bf16 = peaks.get("bf16_tflops_sustained")
-    peak_src = "2 x MEASURED_PEAKS.bf16_tflops_sustained (B200 dense int8 = 2 x dense bf16)"
-    if bf16 is None:
-        bf16, peak_src = 1400.0, "2 x fallback 1.4 PFLOP/s sustained bf16 (B200_PROFILING.md)"
-    peak = 2.0 * bf16
+    if dom.endswith("_f16"):
+        peak, peak_src = f16_peak, "measured f16 dense burst (cuBLAS 8192^3, profiles/peaks_int8_f16.json)"
+        if peak is None:
+            peak, peak_src = peaks.get("bf16_tflops") or 1590.0, "MEASURED_PEAKS bf16 burst (f16 = bf16 rate)"
+    else:
+        peak, peak_src = i8_peak, "measured int8 dense burst (cuBLASLt 8192^3, profiles/peaks_int8_f16.json)"
+        if peak is None:
+            peak, peak_src = 2.0 * (peaks.get("bf16_tflops") or 1590.0), "2 x MEASURED_PEAKS bf16 burst"
     achieved = kernels[dom]["achieved_tops"]
     traffic = None
     if os.path.exists(TRAFFIC):
         traffic = json.load(open(TRAFFIC)).get(dom)
-    if dom.endswith("_f16"):
-        peak, peak_src = bf16, peak_src.replace("2 x ", "").replace(" (B200 dense int8 = 2 x dense bf16)", " (dense f16 = dense bf16)")
-        achieved = kernels[dom]["achieved_tops"]
+    for name, rec in kernels.items():   # every GEMM's fraction of its kind's peak
+        if "achieved_tops" in rec:
+            pk = f16_peak if name.endswith("_f16") else i8_peak
+            if pk:
+                rec["frac_of_peak"] = round(rec["achieved_tops"] / pk, 4)
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "ops_per_launch": ops[dom]}
+                "ops_per_launch": ops[dom],
+                "step_frac": round(step_ops(wl, lens, H, I, L) / (job_ms / args.steps * 1e-3) / 1e12 / peak, 4)}
 
     # ---------------- self-adaptive sweep (configs[2]; reference allocator.build_profile,
     # allocator.py:265-306): every prefix plan k = 0, 2, ..., L of each mode on this batch,

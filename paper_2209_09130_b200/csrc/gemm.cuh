@@ -277,6 +277,13 @@ __device__ __forceinline__ void stage_floats(float* dst, const float* src, int n
 }
 
 // ------------------------------------------------------------------ epilogues
+// SAMP_BIAS_GLOBAL: the QKV / FFN1 epilogues read their bias row straight from global
+// memory (L1-resident, a warp reads one 64-byte span) instead of a per-tile smem copy, so
+// the persistent kernel needs no per-tile barrier among its epilogue warps to recycle the
+// smem copy and the warps drift independently between tiles.
+#ifndef SAMP_BIAS_GLOBAL
+#define SAMP_BIAS_GLOBAL 0
+#endif
 // Interface: smem_bytes<BN>(); prefetch<BN>(params, smem, m0, n0, M, tid, nthreads) runs in
 // the epilogue warps while the main loop is in flight; run<BN, CLUSTER, NE>(params, ctx, smem).
 
@@ -344,6 +351,7 @@ struct EpiSplitKAdd {
 // Fused QKV: per column block (q|k|v) dequant F32(acc)*F32(s_in*s_w) + bias, quantize
 // at the block's site (reference encoder.py:355-366).
 struct EpiQKV {
+  static constexpr bool kStagedBias = !SAMP_BIAS_GLOBAL;   // tile bias copied to smem per tile
   struct Params {
     int8_t* out;          // [M][ldo]
     int ldo;
@@ -371,7 +379,8 @@ struct EpiQKV {
       uint32_t r[32];
       tmem_ld32(c.taddr + col, r);
       float b[32];
-      load_smem32(sbias + c.c0 + col, b);
+      if constexpr (SAMP_BIAS_GLOBAL) load_bias32(p.bias + gcol, b);
+      else load_smem32(sbias + c.c0 + col, b);
       tmem_wait_ld();
       float v[32];
 #pragma unroll
@@ -400,6 +409,7 @@ struct GeluQuantParams {
 };
 template <int MODE>
 struct EpiGeluQuantT {
+  static constexpr bool kStagedBias = !SAMP_BIAS_GLOBAL;
   using Params = GeluQuantParams;
   template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
@@ -442,7 +452,8 @@ struct EpiGeluQuantT {
       float b[CH];
 #pragma unroll
       for (int j = 0; j < CH / 4; ++j) {
-        const float4 v = reinterpret_cast<const float4*>(sbias + c.c0 + col)[j];
+        const float4 v = SAMP_BIAS_GLOBAL ? __ldg(reinterpret_cast<const float4*>(p.bias + gcol) + j)
+                                          : reinterpret_cast<const float4*>(sbias + c.c0 + col)[j];
         b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
       }
       tmem_wait_ld();
@@ -507,6 +518,7 @@ using EpiGeluQuantFast = EpiGeluQuantT<GELU_FAST>;
 // FP16-path bias (+ optional GELU) epilogue: acc(F32) + bias [-> gelu] -> f16 storage.
 // (reference mha_fp encoder.py:291-292 qkv = gemm + qkv_b; ffn_fp :325-326 gelu(mid))
 struct EpiF16Out {
+  static constexpr bool kStagedBias = true;
   struct Params {
     __half* out;
     int ldo;

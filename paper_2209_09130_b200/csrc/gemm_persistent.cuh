@@ -168,7 +168,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
     for (int j = 0; j < my_tiles; ++j) {
       const int b = j & 1;
       // stage tile j+1's bias into the other buffer (its last reader, tile j-1, is done)
-      if (j >= 1 && j + 1 < my_tiles) {
+      if (Epi::kStagedBias && j >= 1 && j + 1 < my_tiles) {
         float* dst = reinterpret_cast<float*>(epi_smem + ((j + 1) & 1) * Lay::EPI_STRIDE + EPI_BIAS_OFF);
         const float* src = ep.bias + tile_n0(j + 1);
         for (int i = ep_tid; i < BN / 4; i += 32 * NE) cp_async16(dst + 4 * i, src + 4 * i);
@@ -185,8 +185,10 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
-      cp_async_wait_all();
-      epi_bar_sync(32 * NE);
+      if constexpr (Epi::kStagedBias) {
+        cp_async_wait_all();
+        epi_bar_sync(32 * NE);
+      }
       if (ep_tid == 0) stamp(j, 2);
     }
   }

@@ -80,7 +80,7 @@ def main():
     import torch
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8192)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "peaks_int8_f16.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "peaks_int8_f16.json"))
     args = ap.parse_args()
     N = args.n
     ops = 2.0 * N ** 3

@@ -252,6 +252,18 @@ def run_sweep(eng, lib, wl, L, nseq, seq_start, att, d_ids, d_segs, head_kind, t
     return res
 
 
+def gather_floats(vals, world, dev, backend) -> list:
+    """every rank's list of floats"""
+    if world == 1:
+        return [list(vals)]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [v.tolist() for v in out]
+
+
 def max_over_ranks_int(x: int, world: int, dev, backend) -> list:
     """every rank's x (all-gather of one int)"""
     if world == 1:
@@ -275,10 +287,15 @@ def run_samp(args):
     if backend != "nccl":
         local = local % max(1, torch.cuda.device_count())
     if world > 1:
+        # communicator evidence in the job log: NCCL prints "comm ... nRanks N" per rank
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        print(f"[bench] rank {rank}/{world} local {local} backend {backend} "
+              f"communicator size {dist.get_world_size()}", file=sys.stderr, flush=True)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -364,9 +381,14 @@ def run_samp(args):
     barrier()
     clocks = ClockSampler(gpu_id).__enter__()
     time.sleep(0.3)
+    barrier()
+    w0 = time.time()
     ms = timed_steps(args.steps, fwd)
+    w1 = time.time()
     barrier()
     job_ms = max_over_ranks(ms)
+    # per-rank device time and wall-clock window of the timed loop (all windows must overlap)
+    per_rank = gather_floats([ms, w0, w1], world, dev, backend)
     value = total_seqs * args.steps / (job_ms / 1e3)
 
     # ---------------- e2e through the public API with host buffers
@@ -527,6 +549,9 @@ def run_samp(args):
             "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches * args.steps, "e2e_text": e2e_text,
             "clocks": clocks.summary(), "latency_b1_p50_ms": lat, "kernels": kernels, "parity": parity,
             "sweep": sweep,
+            "ranks": {"device_ms": [round(r[0], 4) for r in per_rank],
+                      "windows_overlap": bool(max(r[1] for r in per_rank) < min(r[2] for r in per_rank)),
+                      "communicator_size": world},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

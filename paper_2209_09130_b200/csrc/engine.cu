@@ -1161,6 +1161,18 @@ extern "C" int samp_set_site_amax(samp_engine* e, const char* site, double amax)
   return guarded([&] {
     clear_graphs(e);
     e->amax[site] = amax;
+    // admit the FFN1 fast GELU for this ffn.mid scale now (exhaustive ~16 ms device check),
+    // at calibration-load time instead of inside the first forward that needs it
+    const std::string s(site);
+    if (s.size() > 8 && s.compare(s.size() - 8, 8, ".ffn.mid") == 0 && !env_flag("SAMP_NO_GELU_FAST")) {
+      SAMP_CUDA(cudaSetDevice(e->device));
+      const float sm = f32(site_scale(amax));
+      if (!e->gelu_fast_ok.count(bits_of(sm))) {
+        unsigned long long counts[2] = {1, 0};
+        SAMP_CUDA(gelu_fast_check(sm, gelu_inv_s(sm), counts, e->stream));
+        e->gelu_fast_ok[bits_of(sm)] = counts[0] == 0;
+      }
+    }
   });
 }
 

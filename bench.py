@@ -443,6 +443,7 @@ def run_samp(args):
     ops = gemm_ops(T, H, I)
     ops["attention_i8"] = 4 * int((lens ** 2).sum()) * H
     ops["attention_f16"] = 4 * int((lens ** 2).sum()) * H
+    ops["qkv_attention_i8"] = ops["qkv_i8"] + ops["attention_i8"]   # fused QKV GEMM + attention
     # HBM-bound kernels: algorithmic bytes per launch (DESIGN.md kernel table): the embed
     # reads each token's F32 word row and writes its row (int8 on INT8 plans), plus ids /
     # segments / positions; position / type rows and gamma / beta are read once

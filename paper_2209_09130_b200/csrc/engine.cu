@@ -711,16 +711,6 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     qp.sout0 = f32(sc(e, lsite(i, "attn", "q")));
     qp.sout1 = f32(sc(e, lsite(i, "attn", "k")));
     qp.sout2 = f32(sc(e, lsite(i, "attn", "v")));
-    // persistent 128-wide tiles, two CTAs/SM: 35.9k vs 35.8k sentences/s at batch 32 and
-    // batch-1 fully-quant p50 0.525 vs 0.55 ms (twice the CTAs at one row tile)
-    if (!env_flag("SAMP_QKV_ONETILE") && (3 * H) % 128 == 0)
-      check_launch(e, qkv_narrow ? gemm_qkv_i8(-64, a.a_xq[cur], w.m_qkv_i8_64, T, 3 * H, H, qp, st)
-                                 : gemm_qkv_i8(-128, a.a_xq[cur], w.m_qkv_i8_128, T, 3 * H, H, qp, st), "qkv_i8");
-    else
-      check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
-    record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
-    if (e->taps) taps_qkv(e, i, false, a.a_xq[cur], w, qp.mult0, qp.mult1, qp.mult2, 0);
-    for (int k = 0; k < 3; ++k) usage_tap(e, 1 + 8 * i + 1 + k, a.qkv_i8 + k * H, T, H, 3 * H);
     AttnParams ap{};
     ap.ctx_out = a.ctx_i8;
     ap.tile_seq = e->geo.d_tile_seq;
@@ -737,7 +727,38 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     ap.s_ctx = f32(sc(e, lsite(i, "attn", "out_in")));
     ap.tmem_cols = tmem_cols_for_keys(e->geo.max_nkp);
     if (e->usage) ap.hist = e->usage + size_t(1 + 8 * i + 4) * 256;
+    // fused QKV GEMM + attention (qkv_attention.cuh) when every tile's keys fit one 128-row
+    // tile; the code-usage / capture_taps modes keep the two kernels (they tap q|k|v)
+    const bool fused = e->geo.max_nkp <= 128 && H % 128 == 0 && !e->usage && !e->taps &&
+                       !env_flag("SAMP_NO_QA_FUSED");
+    if (fused) {
+      QAParams fq{};
+      fq.att = ap;
+      fq.bias = w.qkv_b;
+      fq.mult0 = qp.mult0;
+      fq.mult1 = qp.mult1;
+      fq.mult2 = qp.mult2;
+      fq.sout0 = qp.sout0;
+      fq.sout1 = qp.sout1;
+      fq.sout2 = qp.sout2;
+      fq.qkv_out = e->capture ? a.qkv_i8 : nullptr;
+      fq.heads = e->d.num_heads;
+      fq.ntiles = e->geo.ntiles;
+      check_launch(e, launch_qkv_attention(a.a_xq[cur], w.m_qkv_i8_64, fq, e->sms, st), "qkv_attention_i8");
+      record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
+    } else {
+    // persistent 128-wide tiles, two CTAs/SM: 35.9k vs 35.8k sentences/s at batch 32 and
+    // batch-1 fully-quant p50 0.525 vs 0.55 ms (twice the CTAs at one row tile)
+    if (!env_flag("SAMP_QKV_ONETILE") && (3 * H) % 128 == 0)
+      check_launch(e, qkv_narrow ? gemm_qkv_i8(-64, a.a_xq[cur], w.m_qkv_i8_64, T, 3 * H, H, qp, st)
+                                 : gemm_qkv_i8(-128, a.a_xq[cur], w.m_qkv_i8_128, T, 3 * H, H, qp, st), "qkv_i8");
+    else
+      check_launch(e, gemm_qkv_i8(t.bn_qkv, a.a_xq[cur], w.m_qkv_i8, T, 3 * H, H, qp, st), "qkv_i8");
+    record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
+    if (e->taps) taps_qkv(e, i, false, a.a_xq[cur], w, qp.mult0, qp.mult1, qp.mult2, 0);
+    for (int k = 0; k < 3; ++k) usage_tap(e, 1 + 8 * i + 1 + k, a.qkv_i8 + k * H, T, H, 3 * H);
     launch_attention(e, false, ap);
+    }
     if (e->taps) taps_attention(e, i, false, ap, 0);
     record(e, "ctx_q", i, a.ctx_i8, size_t(T) * H);
     usage_tap(e, 1 + 8 * i + 5, a.ctx_i8, T, H, H);

@@ -10,6 +10,7 @@
 #include "gemm.cuh"
 #include "heads.cuh"
 #include "ln_rows.cuh"
+#include "qkv_attention.cuh"
 
 namespace samp {
 
@@ -49,6 +50,9 @@ cudaError_t gemm_f16out(int bn, const CUtensorMap& a, const CUtensorMap& b, int 
 cudaError_t launch_attention_i8(const CUtensorMap& map, const AttnParams& p, int ntiles, int heads, int keys_cap,
                                 cudaStream_t st);
 cudaError_t launch_attention_f16(const CUtensorMap& map, const AttnParams& p, int ntiles, int heads, int keys_cap,
+                                 cudaStream_t st);
+// qkv_attention.cu: fused INT8 QKV GEMM + attention (every tile S <= 128, H % 128 == 0)
+cudaError_t launch_qkv_attention(const CUtensorMap& a, const CUtensorMap& w64, const QAParams& q, int sms,
                                  cudaStream_t st);
 // misc_kernels.cu
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st);

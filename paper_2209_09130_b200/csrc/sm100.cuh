@@ -77,6 +77,18 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
+// non-blocking probe (mbarrier.test_wait never suspends; try_wait may park the thread for a
+// system-dependent time when the phase is incomplete, which an event loop polling several
+// barriers cannot afford)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
 // Long waits (microseconds: a warp waiting for another role's whole phase) back off with
 // __nanosleep so the spinning warp does not take issue slots from the warps doing the
 // work on its SM sub-partition (ncu: 8.5% of the attention kernel's instructions were the
@@ -87,6 +99,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     __nanosleep(ns);
     ns = ns < 512 ? 2 * ns : 512;
   }
+}
+
+// Long waits with a suspend-time hint: the waiting warp is parked by the hardware until the
+// phase completes (or the hint expires) instead of re-issuing try_wait / nanosleep, so
+// waiting warps take no issue slots from the warps sharing their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      " @!P1 bra WAIT_%=;\n}\n"
+      :: "r"(smem_addr(bar)), "r"(parity), "r"(1000000) : "memory");
 }
 
 // ------------------------------------------------------------------ PDL

@@ -494,6 +494,18 @@ def run_samp(args):
                 "ops_per_launch": ops[dom],
                 "step_frac": round(step_ops(wl, lens, H, I, L) / (job_ms / args.steps * 1e-3) / 1e12 / peak, 4)}
 
+    if dom == "qkv_attention_i8":
+        # the fused QKV GEMM + attention kernel is bound by the numpy-exact softmax on the
+        # FMA / MUFU pipes, not by the tensor pipe; report the dominant pure GEMM too
+        gd = max((k for k in prof if k in ops and k != dom and "attention" not in k), key=lambda k: prof[k][0])
+        gpk = f16_peak if gd.endswith("_f16") else i8_peak
+        roofline["note"] = ("dominant kernel = fused QKV GEMM + attention (ops = QKV GEMM + QK^T + PV); its bound is "
+                            "the exact softmax on the FMA/MUFU pipes")
+        roofline["gemm_dominant"] = {"kernel": gd, "achieved": kernels[gd]["achieved_tops"], "peak": gpk,
+                                     "frac": round(kernels[gd]["achieved_tops"] / gpk, 4) if gpk else None,
+                                     "ops_per_launch": ops[gd], "traffic": (json.load(open(TRAFFIC)).get(gd)
+                                                                            if os.path.exists(TRAFFIC) else None)}
+
     # ---------------- self-adaptive sweep (configs[2]; reference allocator.build_profile,
     # allocator.py:265-306): every prefix plan k = 0, 2, ..., L of each mode on this batch,
     # device time per forward and label agreement with the all-FP plan (random weights: no

@@ -173,6 +173,8 @@ struct samp_engine {
   std::vector<int> h_pos;
   bool profiling = false;
   int sms = 148;                  // SM count of the engine's device
+  cudaStream_t side = nullptr;    // L2 weight prefetch runs here, forked from the forward's stream
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // GEMM phase stamps (profiling mode): [stamp_cap launches][STAMP_CTAS][GEMM_STAMPS]
   unsigned long long* stamps = nullptr;
   int stamp_cap = 0;
@@ -958,8 +960,43 @@ static void enqueue_kernels(samp_engine* e, const uint8_t* prec, int nseq, int h
   check_launch(e, launch_embed(ep, st), "embed");
   record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
   tap_record(e, "embed.out", a.hid_f32, size_t(T) * H * 4);
+  // the layers' weights (in use order) into L2 on a side stream while the first layers run;
+  // SAMP_NO_PREFETCH=1 disables it (A/B measurements)
+  // (off in the per-kernel profiling pass, which times kernels one by one)
+  const bool prefetch = !e->exact && !e->profiling && !env_flag("SAMP_NO_PREFETCH");
+  if (prefetch) {
+    if (!e->side) {
+      SAMP_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+      SAMP_CUDA(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
+      SAMP_CUDA(cudaEventCreateWithFlags(&e->join_ev, cudaEventDisableTiming));
+    }
+    PrefetchList pl{};
+    const size_t HH = size_t(H) * H, HI = size_t(H) * d.intermediate;
+    auto add = [&](const void* ptr, size_t bytes) {
+      if (ptr && pl.n < PREFETCH_MAX_RANGES) {
+        pl.ptr[pl.n] = ptr;
+        pl.bytes[pl.n] = bytes;
+        ++pl.n;
+      }
+    };
+    for (int i = 0; i < L; ++i) {
+      const LayerDev& w = e->layers[i];
+      const bool mha8 = prec[i] == SAMP_LAYER_FULL_INT8 || prec[i] == SAMP_LAYER_MHA_INT8;
+      const bool ffn8 = prec[i] == SAMP_LAYER_FULL_INT8 || prec[i] == SAMP_LAYER_FFN_INT8;
+      if (mha8) { add(w.qkv_i8, 3 * HH); add(w.wo_i8, HH); }
+      else { add(w.qkv_f16, 6 * HH); add(w.wo_f16, 2 * HH); }
+      if (ffn8) { add(w.w1_i8, HI); add(w.w2_i8, HI); }
+      else { add(w.w1_f16, 2 * HI); add(w.w2_f16, 2 * HI); }
+    }
+    SAMP_CUDA(cudaEventRecord(e->fork_ev, st));
+    SAMP_CUDA(cudaStreamWaitEvent(e->side, e->fork_ev, 0));
+    SAMP_REQUIRE(launch_l2_prefetch(pl, 32, e->side) == cudaSuccess, SAMP_E_DEVICE, "l2_prefetch launch failed");
+    e->launches++;
+    SAMP_CUDA(cudaEventRecord(e->join_ev, e->side));
+  }
   int cur = 0;
   for (int i = 0; i < L; ++i) run_layer(e, i, prec, cur);
+  if (prefetch) SAMP_CUDA(cudaStreamWaitEvent(st, e->join_ev, 0));
   // ---------------- heads + outputs (final hidden is always F32 in hid_f32)
   const int nl = d.num_labels;
   if (head != SAMP_HEAD_NONE) {
@@ -1028,6 +1065,9 @@ extern "C" void samp_engine_destroy(samp_engine* e) {
   clear_graphs(e);
   if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
   if (e->pinned_out) cudaFreeHost(e->pinned_out);
+  if (e->side) cudaStreamDestroy(e->side);
+  if (e->fork_ev) cudaEventDestroy(e->fork_ev);
+  if (e->join_ev) cudaEventDestroy(e->join_ev);
   cudaStreamDestroy(e->stream);
   delete e;
 }

@@ -55,6 +55,15 @@ cudaError_t launch_attention_f16(const CUtensorMap& map, const AttnParams& p, in
 cudaError_t launch_qkv_attention(const CUtensorMap& a, const CUtensorMap& w64, const QAParams& q, int sms,
                                  cudaStream_t st);
 // misc_kernels.cu
+// L2 weight prefetch (side stream): the byte ranges are prefetched in list order in 32 KB
+// chunks with cp.async.bulk.prefetch.L2 (no data reaches the SM)
+constexpr int PREFETCH_MAX_RANGES = 128;
+struct PrefetchList {
+  const void* ptr[PREFETCH_MAX_RANGES];
+  unsigned long long bytes[PREFETCH_MAX_RANGES];
+  int n;
+};
+cudaError_t launch_l2_prefetch(const PrefetchList& l, int ctas, cudaStream_t st);
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t st);
 cudaError_t launch_ln_rows(const LnRowsParams& p, int hidden, cudaStream_t st);
 bool ln_rows_supported(int hidden);

@@ -4,6 +4,33 @@
 
 namespace samp {
 
+// Weight ranges of the forward, in use order, pulled into L2 while the first layers run
+// (the timed forward starts with a cold L2; small batches stream each weight tile through a
+// handful of SMs, so their main loops wait on HBM latency).  Chunk c of the flattened list
+// goes to CTA c % gridDim.x, so the early layers' chunks are issued first.
+__global__ void l2_prefetch_kernel(const __grid_constant__ PrefetchList l) {
+  constexpr unsigned long long CHUNK = 32768;
+  if (threadIdx.x != 0) return;
+  unsigned long long base = 0;   // first chunk index of range i
+  for (int i = 0; i < l.n; ++i) {
+    const unsigned long long nch = (l.bytes[i] + CHUNK - 1) / CHUNK;
+    unsigned long long c = (blockIdx.x + gridDim.x - base % gridDim.x) % gridDim.x;   // my first chunk of range i
+    for (; c < nch; c += gridDim.x) {
+      const unsigned long long off = c * CHUNK;
+      const unsigned long long sz = l.bytes[i] - off < CHUNK ? l.bytes[i] - off : CHUNK;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                   :: "l"(reinterpret_cast<const char*>(l.ptr[i]) + off), "r"(unsigned(sz & ~15ull)) : "memory");
+    }
+    base += nch;
+  }
+}
+
+cudaError_t launch_l2_prefetch(const PrefetchList& l, int ctas, cudaStream_t st) {
+  max_carveout_once(l2_prefetch_kernel);
+  l2_prefetch_kernel<<<ctas, 32, 0, st>>>(l);
+  return cudaGetLastError();
+}
+
 template <int H>
 static cudaError_t embed_h(const EmbedParams& p, cudaStream_t st) {
   static thread_local int configured = -1;

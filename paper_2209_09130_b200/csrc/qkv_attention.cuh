@@ -24,8 +24,7 @@
 //               (accumulator -> q|k|v codes in the 64B-swizzled K-major layout the MMAs read,
 //               double-buffered in smem; it runs while MMA-2 of the current item computes),
 //               then the softmax (att_softmax_rr) and the ctx codes (att_ctx_out)
-// TMEM columns: q|k|v accumulators [0, 192) and [320, 512), scores [192, 320) (O = P.V
-// reuses its first 64 columns).
+// TMEM columns: q|k|v accumulator [0, 192), scores [256, 384), O [384, 448).
 #pragma once
 #include "attention.cuh"
 #include "gemm.cuh"
@@ -50,9 +49,9 @@ struct QALayout {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;     // + alignment slack
   static_assert(QKV_OFF % 1024 == 0 && P_OFF % 1024 == 0, "swizzle atoms need 1024-byte alignment");
 };
-// TMEM columns: two q|k|v accumulators (GEMM(j+1) runs while the epilogue drains j) and the
-// scores; O = P.V reuses the first 64 score columns once pass 3 has read them
-constexpr uint32_t QA_TMEM_ACC0 = 0, QA_TMEM_S = 192, QA_TMEM_ACC1 = 320, QA_TMEM_O = QA_TMEM_S;
+// TMEM columns: the q|k|v accumulator, the scores and O = P.V each have their own columns,
+// so MMA-1 of the next item (into the scores) never waits for this item's ctx (reading O)
+constexpr uint32_t QA_TMEM_ACC = 0, QA_TMEM_S = 256, QA_TMEM_O = 384;
 
 struct QAParams {
   AttnParams att;          // ctx output, tiles, sequence geometry, softmax / ctx scales
@@ -72,14 +71,13 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
   uint64_t* empty = full + QA_STAGES;
-  uint64_t* acc_full = empty + QA_STAGES;   // [2]
-  uint64_t* acc_empty = acc_full + 2;       // [2]
-  uint64_t* qkv_full = acc_empty + 2;    // [2]
+  uint64_t* acc_full = empty + QA_STAGES;
+  uint64_t* acc_empty = acc_full + 1;
+  uint64_t* qkv_full = acc_empty + 1;    // [2]
   uint64_t* s_full = qkv_full + 2;
   uint64_t* p_full = s_full + 1;
   uint64_t* o_full = p_full + 1;
-  uint64_t* o_free = o_full + 1;         // ctx(j) read O: the score columns may be rewritten
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const AttnParams& p = q.att;
   const int H = p.hidden;
@@ -107,15 +105,12 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4 * TPR);
-      mbar_init(&qkv_full[b], 128 * TPR);
-    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4 * TPR);
+    for (int b = 0; b < 2; ++b) mbar_init(&qkv_full[b], 128 * TPR);
     mbar_init(s_full, 1);
     mbar_init(p_full, 128 * TPR);
     mbar_init(o_full, 1);
-    mbar_init(o_free, 4 * TPR);
     fence_barrier_init();
   }
   if (warp == 0 && elect_one()) {
@@ -182,8 +177,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
           mma_commit(o_full);
           ++m2;
           did = true;
-        } else if (m1 == m2 && m1 < g && mbar_test(&qkv_full[m1 & 1], (m1 >> 1) & 1) &&
-                   (m1 == 0 || mbar_test(o_free, (m1 - 1) & 1))) {
+        } else if (m1 == m2 && m1 < g && mbar_test(&qkv_full[m1 & 1], (m1 >> 1) & 1)) {
           tc_fence_after();
           const int b = m1 & 1;
           const int nkp = tile_keys(item_tile(m1));
@@ -199,23 +193,22 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
           did = true;
         } else if (g < my && g <= m1 &&   // GEMM(j+1) only after MMA-1(j): MMAs run in issue order,
                                             // so queued GEMM work would delay the scores the softmax waits for
-                   (gkb > 0 || mbar_test(&acc_empty[g & 1], ((g >> 1) & 1) ^ 1)) &&
+                   (gkb > 0 || mbar_test(acc_empty, (g & 1) ^ 1)) &&
                    mbar_test(&full[it % QA_STAGES], (it / QA_STAGES) & 1)) {
           // one k-block of GEMM(g): acc[128 x 192] = A rows . [Wq | Wk | Wv] head slices
           tc_fence_after();
           if (gkb == 0 && rec(g)) rec(g)[10] = globaltimer();
           const int s = it % QA_STAGES;
-          const uint32_t acc = (g & 1) ? QA_TMEM_ACC1 : QA_TMEM_ACC0;
           const uint32_t a_base = smem_addr(smem + s * Lay::STAGE);
           const uint32_t b_base = a_base + Lay::A_BYTES;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_ss<KIND_I8>(tmem + acc, sdesc_k_sw128(a_base + 32 * k), sdesc_k_sw128(b_base + 32 * k), IDESC_QKV,
+            mma_ss<KIND_I8>(tmem + QA_TMEM_ACC, sdesc_k_sw128(a_base + 32 * k), sdesc_k_sw128(b_base + 32 * k), IDESC_QKV,
                             (gkb | k) != 0);
           mma_commit(&empty[s]);
           ++it;
           if (++gkb == nk) {
-            mma_commit(&acc_full[g & 1]);
+            mma_commit(acc_full);
             if (rec(g)) rec(g)[11] = globaltimer();
             gkb = 0;
             ++g;
@@ -244,10 +237,10 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     auto epilogue = [&](int jj, unsigned long long* st) {
       const int b = jj & 1;
       if (st) st[0] = globaltimer();
-      mbar_wait_park(&acc_full[b], (jj >> 1) & 1);
+      mbar_wait_park(acc_full, jj & 1);
       tc_fence_after();
       if (st) st[1] = globaltimer();
-      const uint32_t ta = tmem + (b ? QA_TMEM_ACC1 : QA_TMEM_ACC0) + lane_base + h * CW;
+      const uint32_t ta = tmem + QA_TMEM_ACC + lane_base + h * CW;
       uint32_t u[3][CW];
 #pragma unroll
       for (int blk = 0; blk < 3; ++blk) {
@@ -257,7 +250,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&acc_empty[b]);   // the accumulator is in registers
+      if (lane_id() == 0) mbar_arrive(acc_empty);   // the accumulator is in registers
       const int t = item_tile(jj), head = item_head(jj);
       const int seq = p.tile_seq[t];
       const int row0 = p.seq_start[seq];
@@ -322,10 +315,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       att_ctx_out<false, TPR>(p, w, tmem + QA_TMEM_O + lane_base, size_t(p.seq_start[seq] + r), head, 0.0f);
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) {
-        mbar_arrive(o_free);
-        if (rec(j)) atomicMax(rec(j) + 13, globaltimer());   // last warp's ctx
-      }
+      if (lane_id() == 0 && rec(j)) atomicMax(rec(j) + 13, globaltimer());   // last warp's ctx
       if (st) st[9] = globaltimer();
     }
   }

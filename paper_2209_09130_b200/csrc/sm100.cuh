@@ -307,9 +307,24 @@ inline bool pdl_enabled() {
 }
 
 // cudaLaunchKernelEx with programmatic stream serialization (+ optional cluster dims)
+// Every hot-path kernel asks for the maximum shared-memory carveout: kernels that would
+// otherwise get different L1/shared splits force the SMs to drain and reconfigure between
+// consecutive launches (SAMP_NO_CARVEOUT=1 leaves the driver's choice, A/B only).
+template <class K>
+inline void max_carveout_once(K* kern) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured == dev) return;
+  configured = dev;
+  if (std::getenv("SAMP_NO_CARVEOUT") == nullptr)
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared));
+}
+
 template <class... KArgs, class... Args>
 inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              int cluster_x, Args&&... args) {
+  max_carveout_once(kern);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

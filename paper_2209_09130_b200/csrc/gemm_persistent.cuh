@@ -24,12 +24,6 @@
 
 namespace samp {
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr(smem_dst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int BN, int STAGES, int EPI_BYTES>
 struct PersistLayout {
@@ -48,7 +42,8 @@ struct PersistLayout {
 template <int KIND, int BN, int STAGES, int NE, class Epi, int CTAS = 1>
 __global__ void __launch_bounds__(64 + 32 * NE, CTAS)
 gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                       int M, int N, int k_bytes, const typename Epi::Params ep, unsigned long long* stamps) {
+                       int M, int N, int k_bytes, const typename Epi::Params ep, unsigned long long* stamps,
+                       int n_fastest) {
   using Lay = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
   constexpr int TMEM_COLS = tmem_cols_for(2 * BN);
   constexpr int PARTS = NE / 4;
@@ -72,8 +67,18 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
   const int ntiles = mtiles * (N / BN);
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
   const int nk = k_bytes / 128;
-  auto tile_m0 = [&](int j) { return ((int(blockIdx.x) + j * int(gridDim.x)) % mtiles) * GEMM_BM; };
-  auto tile_n0 = [&](int j) { return ((int(blockIdx.x) + j * int(gridDim.x)) / mtiles) * BN; };
+  // raster: row tiles fastest (the CTAs running together share a weight tile; small M), or,
+  // when the activation rows do not stay in L2 (n_fastest), weight tiles fastest so every
+  // row tile is read from HBM once and the weights (<= a few MB) are the L2-resident operand
+  const int ntn = N / BN;
+  auto tile_m0 = [&](int j) {
+    const int t = int(blockIdx.x) + j * int(gridDim.x);
+    return (n_fastest ? t / ntn : t % mtiles) * GEMM_BM;
+  };
+  auto tile_n0 = [&](int j) {
+    const int t = int(blockIdx.x) + j * int(gridDim.x);
+    return (n_fastest ? t % ntn : t / mtiles) * BN;
+  };
   // phase stamps (measurement): CTA b < 64, tile j < 16 -> stamps[(b*16 + j)*8 + f]:
   // f0 epilogue starts waiting, f1 accumulator ready, f2 epilogue done, f3 MMA starts
   // (buffer free), f4 last MMA of the tile issued, f5 producer issues the tile's first box
@@ -228,8 +233,11 @@ inline cudaError_t launch_gemm_persistent(const CUtensorMap& map_a, const CUtens
   const int slots = device_sm_count() * CTAS;
   const int grid = tiles < slots ? tiles : slots;
   unsigned long long* stamps = g_gemm_stamps;
+  // activations past ~48 MB (C5: 262k tokens) would be streamed from HBM once per weight
+  // tile with row tiles fastest (ncu: FFN1 read 6.3 GB for a 201 MB input)
+  const int n_fastest = size_t(M) * size_t(k_bytes) > (48u << 20) ? 1 : 0;
   return launch_ex(kern, dim3(grid), dim3(64 + 32 * NE), Lay::TOTAL, stream, 1, map_a, map_b, M, N, k_bytes, p,
-                   stamps);
+                   stamps, n_fastest);
 }
 
 }  // namespace samp

@@ -960,10 +960,11 @@ static void enqueue_kernels(samp_engine* e, const uint8_t* prec, int nseq, int h
   check_launch(e, launch_embed(ep, st), "embed");
   record(e, "embed_f32", 0, a.hid_f32, size_t(T) * H * 4);
   tap_record(e, "embed.out", a.hid_f32, size_t(T) * H * 4);
-  // the layers' weights (in use order) into L2 on a side stream while the first layers run;
-  // SAMP_NO_PREFETCH=1 disables it (A/B measurements)
-  // (off in the per-kernel profiling pass, which times kernels one by one)
-  const bool prefetch = !e->exact && !e->profiling && !env_flag("SAMP_NO_PREFETCH");
+  // SAMP_PREFETCH=1: the layers' weights (in use order) into L2 on a side stream while the
+  // first layers run.  Opt-in: measured neutral (C2 and every batch-1 mode within noise,
+  // DESIGN.md) — the small-batch kernels are not waiting on HBM.  Never in the per-kernel
+  // profiling pass, which times kernels one by one.
+  const bool prefetch = !e->exact && !e->profiling && env_flag("SAMP_PREFETCH");
   if (prefetch) {
     if (!e->side) {
       SAMP_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));

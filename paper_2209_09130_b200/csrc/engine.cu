@@ -138,6 +138,8 @@ struct Activations {
   CUtensorMap a_xq[2], a_ctx_i8, a_ffn_in, a_mid_i8, a_hid_f16, a_ctx_f16, a_ln1_f16, a_mid_f16;
   CUtensorMap a_ctx_i8_mc[2], a_mid_i8_mc[2];   // 32- / 16-row boxes (A multicast in 4- / 8-CTA clusters)
   CUtensorMap att_qkv_i8, att_qkv_f16;
+  // LN-GEMM outputs stored by TMA (one box of bn_ln columns x 128 rows, no swizzle)
+  CUtensorMap st_ffn_in, st_xq[2];
 };
 
 struct Geometry {
@@ -275,6 +277,11 @@ static void ensure_activations(samp_engine* e, int T) {
   // attention: one head row (64 int8 / 64 f16) x 64 rows
   a.att_qkv_i8 = tmap_i8(a.qkv_i8, cap, 3 * H, 3 * H, 64, 64, CU_TENSOR_MAP_SWIZZLE_64B);
   a.att_qkv_f16 = tmap_f16(a.qkv_f16, cap, 3 * H, 3 * H, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e->tiles.bn_ln && e->tiles.bn_ln <= 256) {
+    a.st_ffn_in = tmap_i8(a.ffn_in_i8, cap, H, H, e->tiles.bn_ln, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.st_xq[0] = tmap_i8(a.xq[0], cap, H, H, e->tiles.bn_ln, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.st_xq[1] = tmap_i8(a.xq[1], cap, H, H, e->tiles.bn_ln, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
 }
 
 static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, const int32_t* att_len) {
@@ -774,6 +781,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.eps = eps;
     lp.hidden = H;
     lp.out_i8 = a.ffn_in_i8;
+    lp.out_map = a.st_ffn_in;   // used by the TMA-store epilogue (gemm_ln_i8 decides)
     lp.s_out = f32(sc(e, lsite(i, "ffn", "in")));
     if (p == SAMP_LAYER_MHA_INT8) {  // FP FFN consumes dequant(ffn.in codes)
       lp.deq_outputs = 1;
@@ -864,6 +872,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   lp.bias = w.b2;
   if (next_int8) {
     lp.out_i8 = a.xq[cur ^ 1];
+    lp.out_map = a.st_xq[cur ^ 1];
     lp.s_out = f32(sc(e, input_site(i + 1)));
     if (e->taps) lp.tap_f32 = e->tap_ln;   // attn.in of the next layer, before its quantize
   } else {

@@ -28,11 +28,15 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
   const bool i8_only = p.res_i8 && !p.acc_is_f32 && p.out_i8 && !p.deq_outputs && !p.f16_round && !p.amax &&
                        !p.out_f32 && !p.out_f16 && !p.tap_f32;
   if (i8_only) {
+    // the code tile leaves through one TMA store per CTA (out_map: box bn_ln x 128) instead of
+    // 16-byte row-strided stores (32 rows per warp instruction); SAMP_NO_LN_TMA_STORE=1: A/B
+    EpiResLN::Params q = p;
+    q.tma_store = env_flag("SAMP_NO_LN_TMA_STORE") ? 0 : 1;
     switch (t.bn_ln * 10 + t.cluster_ln) {
       case 1924:
-        if (mc) return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8, true>(a_mc[0], b, M, N, kb, p, st);
-        return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
-      case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLNI8>(a, b, M, N, kb, p, st);
+        if (mc) return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8, true>(a_mc[0], b, M, N, kb, q, st);
+        return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8>(a, b, M, N, kb, q, st);
+      case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLNI8>(a, b, M, N, kb, q, st);
     }
   }
   switch (t.bn_ln * 10 + t.cluster_ln) {

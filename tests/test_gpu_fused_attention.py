@@ -132,3 +132,31 @@ def test_fused_equals_unfused(base2, monkeypatch, specs):
     fused = _run(arch, encs, plan, monkeypatch, True)
     ref = _run(arch, encs, plan, monkeypatch, False)
     np.testing.assert_array_equal(fused, ref)
+
+
+def test_fused_bert_large_geometry(monkeypatch):
+    """H = 1024, 16 heads (BERT-large widths; K = 8 k-blocks, 3H biases in smem), S <= 128."""
+    vocab = tiny_vocab(max_seq_len=512, extra_tokens=[f"w{i}" for i in range(1000 - 44)])
+    arch = build_archive(num_layers=2, hidden=1024, num_heads=16, intermediate=4096, max_position=512, seed=9,
+                         weight_scale=0.02, vocab=vocab, task="classification")
+    model = orc.Model.from_manifest(arch.manifest, arch.tensors)
+    table = CalibrationTable(model_fingerprint=arch.fingerprint)
+    rng = np.random.default_rng(8)
+    ids = rng.integers(4, 1000, 100).tolist()
+    taps = {}
+    orc.run(model, ids, [0] * len(ids), len(ids), orc.plan_prefix("FP", 2, 0), taps=taps)
+    for site, v in taps.items():
+        table.observe(site, v)
+    arch.calibration = table
+    amax = {s: e.amax for s, e in table.entries.items()}
+    encs = _batch(np.random.default_rng(12), [(128, 128), (128, 70), (64, 64), (64, 64), (96, 96)] * 3)
+    plan = PrecisionPlan.prefix("FULLY_QUANT", 2, 2)
+    fused = _run(arch, encs, plan, monkeypatch, True)
+    ref = _run(arch, encs, plan, monkeypatch, False)
+    np.testing.assert_array_equal(fused, ref)
+    model = orc.Model.from_manifest(arch.manifest, arch.tensors, amax)
+    seq_start = np.concatenate([[0], np.cumsum([len(e.token_ids) for e in encs])])
+    for s in (0, 1, 4):
+        e = encs[s]
+        want = orc.run(model, e.token_ids, e.segment_ids, e.attention_length, plan.layer_precisions)
+        np.testing.assert_array_equal(fused[seq_start[s]:seq_start[s + 1]], want)

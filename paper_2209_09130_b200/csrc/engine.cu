@@ -140,6 +140,7 @@ struct Activations {
   CUtensorMap att_qkv_i8, att_qkv_f16;
   // LN-GEMM outputs stored by TMA (one box of bn_ln columns x 128 rows, no swizzle)
   CUtensorMap st_ffn_in, st_xq[2];
+  CUtensorMap st_small_ffn_in, st_small_xq[2];   // small batches: box bn_ln_small x 128
 };
 
 struct Geometry {
@@ -281,6 +282,12 @@ static void ensure_activations(samp_engine* e, int T) {
     a.st_ffn_in = tmap_i8(a.ffn_in_i8, cap, H, H, e->tiles.bn_ln, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
     a.st_xq[0] = tmap_i8(a.xq[0], cap, H, H, e->tiles.bn_ln, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
     a.st_xq[1] = tmap_i8(a.xq[1], cap, H, H, e->tiles.bn_ln, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
+  if (e->tiles.bn_ln_small && e->tiles.bn_ln_small <= 256) {
+    const uint32_t bs = e->tiles.bn_ln_small;
+    a.st_small_ffn_in = tmap_i8(a.ffn_in_i8, cap, H, H, bs, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.st_small_xq[0] = tmap_i8(a.xq[0], cap, H, H, bs, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.st_small_xq[1] = tmap_i8(a.xq[1], cap, H, H, bs, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
 }
 
@@ -781,7 +788,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.eps = eps;
     lp.hidden = H;
     lp.out_i8 = a.ffn_in_i8;
-    lp.out_map = a.st_ffn_in;   // used by the TMA-store epilogue (gemm_ln_i8 decides)
+    lp.out_map = ln_small ? a.st_small_ffn_in : a.st_ffn_in;   // TMA-store epilogue (gemm_ln_i8 decides)
     lp.s_out = f32(sc(e, lsite(i, "ffn", "in")));
     if (p == SAMP_LAYER_MHA_INT8) {  // FP FFN consumes dequant(ffn.in codes)
       lp.deq_outputs = 1;
@@ -872,7 +879,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   lp.bias = w.b2;
   if (next_int8) {
     lp.out_i8 = a.xq[cur ^ 1];
-    lp.out_map = a.st_xq[cur ^ 1];
+    lp.out_map = ln_small ? a.st_small_xq[cur ^ 1] : a.st_xq[cur ^ 1];
     lp.s_out = f32(sc(e, input_site(i + 1)));
     if (e->taps) lp.tap_f32 = e->tap_ln;   // attn.in of the next layer, before its quantize
   } else {

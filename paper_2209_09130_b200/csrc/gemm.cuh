@@ -1033,18 +1033,46 @@ struct EpiResLNT {
       return __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
     };
     const float hf = float(p.hidden);
-    const float total = reduce_row<BN, CLUSTER, NE>(half_leaf([](float v) { return v; }), c, halves, smem, 0);
+    if (c.sub) c.sub[0] = globaltimer();
+    const float lsum = half_leaf([](float v) { return v; });
+    if (c.sub) c.sub[1] = globaltimer();
+    const float total = reduce_row<BN, CLUSTER, NE>(lsum, c, halves, smem, 0);
     const float mean = __fdiv_rn(__fadd_rn(0.0f, total), hf);
-    const float total2 = reduce_row<BN, CLUSTER, NE>(half_leaf([mean](float v) {
-                                                   const float d = __fsub_rn(v, mean);
-                                                   return __fmul_rn(d, d);
-                                                 }),
-                                                 c, halves, smem, 1);
+    if (c.sub) c.sub[2] = globaltimer();
+    const float lsum2 = half_leaf([mean](float v) {
+      const float d = __fsub_rn(v, mean);
+      return __fmul_rn(d, d);
+    });
+    if (c.sub) c.sub[3] = globaltimer();
+    const float total2 = reduce_row<BN, CLUSTER, NE>(lsum2, c, halves, smem, 1);
     const float var = __fdiv_rn(__fadd_rn(0.0f, total2), hf);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
     const Recip rq = make_recip(p.out_i8 || p.deq_outputs ? p.s_out : 1.0f);
+    if (c.sub) c.sub[4] = globaltimer();
     float amx = 0.0f;
-    if (valid) {
+    if constexpr (I8_ONLY) {
+      // int8-only chain: normalise + quantize on FFMA2 pairs, γ/β as float4 (same roundings)
+      const X2 kx = p.k;
+      const float2 nm = f2(-mean, -mean), iv = f2(inv, inv);
+#pragma unroll
+      for (int g = 0; g < 12; ++g) {
+        const int col = 8 * g + jo;
+        const float4 g4 = *reinterpret_cast<const float4*>(sgam + col);
+        const float4 b4 = *reinterpret_cast<const float4*>(sbet + col);
+        float2 q[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float2 y = mul2(mul2(add2(f2(x[4 * g + 2 * u], x[4 * g + 2 * u + 1]), nm, kx), iv, kx),
+                          u ? f2(g4.z, g4.w) : f2(g4.x, g4.y), kx);
+          y = add2(y, u ? f2(b4.z, b4.w) : f2(b4.x, b4.y), kx);
+          y = f2(fminf(fmaxf(y.x, -1.8446744e19f), 1.8446744e19f), fminf(fmaxf(y.y, -1.8446744e19f), 1.8446744e19f));
+          q[u] = quant_pre2(y, rq, kx);
+        }
+        const uint32_t codes = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
+        if (p.tma_store) *reinterpret_cast<uint32_t*>(c.stage + size_t(c.tile_row) * BN + col) = codes;
+        else if (valid) *reinterpret_cast<uint32_t*>(p.out_i8 + rbase + c.n0 + col) = codes;
+      }
+    } else if (valid) {
 #pragma unroll
       for (int g = 0; g < 12; ++g) {
         const int col = 8 * g + jo;
@@ -1066,9 +1094,10 @@ struct EpiResLNT {
 #pragma unroll
           for (int u = 0; u < 4; ++u) y[u] = deq(q[u], p.s_out);
         } else if (p.out_i8) {
-          *reinterpret_cast<uint32_t*>(p.out_i8 + o) =
-              trunc_pack4_s8(quant_pre_fast(y[0], rq), quant_pre_fast(y[1], rq), quant_pre_fast(y[2], rq),
-                             quant_pre_fast(y[3], rq));
+          const uint32_t codes = trunc_pack4_s8(quant_pre_fast(y[0], rq), quant_pre_fast(y[1], rq),
+                                                quant_pre_fast(y[2], rq), quant_pre_fast(y[3], rq));
+          if (p.tma_store) *reinterpret_cast<uint32_t*>(c.stage + size_t(c.tile_row) * BN + col) = codes;
+          else *reinterpret_cast<uint32_t*>(p.out_i8 + o) = codes;
         }
         if (p.amax) {
 #pragma unroll
@@ -1082,6 +1111,16 @@ struct EpiResLNT {
         }
       }
     }
+    if (p.tma_store) {   // int8-only chain: the [128][96] code tile leaves by one TMA store
+      fence_proxy_async_smem();
+      epi_bar_sync(c.ne_threads);
+      if (c.ep_tid == 0) {
+        tma_store_2d(&p.out_map, c.stage, c.n0, c.row - c.tile_row);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+    }
+    if (c.sub) c.sub[5] = globaltimer();
     if (p.amax) {
       amax_commit(p.amax + p.site, amx);
       if (p.site2 >= 0) amax_commit(p.amax + p.site2, amx);

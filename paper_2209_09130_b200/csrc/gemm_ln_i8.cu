@@ -52,12 +52,18 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
     // small batches: 8-CTA clusters; each CTA streams K x 96 weights alone, so the ring
     // depth sets the bytes in flight (batch-1 fully-quant p50 0.474 vs 0.507 ms at 4 stages;
     // 7 stages no better)
-    case 968:
+    case 968: {
       // two epilogue threads per row, numpy's accumulators split by index (run_strided):
       // batch-1 fully-quant p50 0.469 -> 0.454 ms vs one thread per row
       if (mc) return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN, true>(a_mc[1], b, M, N, kb, p, st);
       if (env_flag("SAMP_NO_LN96_STRIDED")) return launch_gemm<KIND_I8, 96, 6, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
+      if (i8_only) {   // int8-only chain: compact paired epilogue, codes out by one TMA store
+        EpiResLN::Params q = p;
+        q.tma_store = env_flag("SAMP_NO_LN_TMA_STORE") ? 0 : 1;
+        return launch_gemm<KIND_I8, 96, 6, 8, 8, EpiResLNI8>(a, b, M, N, kb, q, st);
+      }
       return launch_gemm<KIND_I8, 96, 6, 8, 8, EpiResLN>(a, b, M, N, kb, p, st);
+    }
     case 1288: return launch_gemm<KIND_I8, 128, 5, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
   }
   return cudaErrorInvalidValue;

@@ -141,6 +141,8 @@ struct Activations {
   // LN-GEMM outputs stored by TMA (one box of bn_ln columns x 128 rows, no swizzle)
   CUtensorMap st_ffn_in, st_xq[2];
   CUtensorMap st_small_ffn_in, st_small_xq[2];   // small batches: box bn_ln_small x 128
+  // small-batch FP LN outputs by TMA (box 32 x 128; f32 128B swizzle, f16 64B swizzle)
+  CUtensorMap st_ln1_f32, st_ln1_f16, st_hid_f32, st_hid_f16;
 };
 
 struct Geometry {
@@ -289,6 +291,12 @@ static void ensure_activations(samp_engine* e, int T) {
     a.st_small_xq[0] = tmap_i8(a.xq[0], cap, H, H, bs, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
     a.st_small_xq[1] = tmap_i8(a.xq[1], cap, H, H, bs, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
+  a.st_ln1_f32 = make_tmap_2d(a.ln1_f32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cap, H, size_t(H) * 4, 32, 128,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+  a.st_hid_f32 = make_tmap_2d(a.hid_f32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cap, H, size_t(H) * 4, 32, 128,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+  a.st_ln1_f16 = tmap_f16(a.ln1_f16, cap, H, H, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+  a.st_hid_f16 = tmap_f16(a.hid_f16, cap, H, H, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, const int32_t* att_len) {
@@ -841,6 +849,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     EpiResLN::Params lp{};
     lp.bias = w.ob;
     lp.res_f32 = a.hid_f32;
+    lp.map_res = a.st_hid_f32;   // small-batch TMA-loaded residual (gemm_ln_f16 decides)
     lp.gamma = w.ln1_g;
     lp.beta = w.ln1_b;
     lp.acc_is_f32 = 1;
@@ -852,6 +861,8 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     } else {
       lp.out_f32 = a.ln1_f32;
       lp.out_f16 = a.ln1_f16;
+      lp.map_f32 = a.st_ln1_f32;   // small-batch TMA-store epilogue (gemm_ln_f16 decides)
+      lp.map_f16 = a.st_ln1_f16;
       lp.f16_round = fp16_store;
       lp.amax = cal;
       lp.site = cbase + 6;
@@ -921,6 +932,9 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     if (e->taps) taps_ffn_mid(e, i, true, a.a_ln1_f16, w, 1.0f, p == SAMP_LAYER_FP ? fp16_store : 0);
     lp.res_f32 = a.ln1_f32;
     lp.acc_is_f32 = 1;
+    lp.map_f32 = a.st_hid_f32;
+    lp.map_f16 = a.st_hid_f16;
+    lp.map_res = a.st_ln1_f32;
     lp.f16_round = (p == SAMP_LAYER_FP) ? fp16_store : 0;
     if (e->calib_amax && i + 1 < L) {   // tap L{i+1}.attn.in
       lp.amax = e->calib_amax;

@@ -26,6 +26,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "numerics.cuh"
 #include "sm100.cuh"
 
@@ -64,7 +66,13 @@ struct EpiCtx {
   int ne_threads;    // 32*NE
   unsigned long long* sub = nullptr;   // measurement: epilogue sub-phase stamps (thread 0 only)
   uint8_t* stage = nullptr;            // free smem (the drained operand ring) for a TMA-stored tile
+  uint8_t* ring = nullptr;             // the operand ring's A slots (TMA-loaded residual boxes)
+  int res_slot0 = 0, stages = 1;       // residual box k sits in A slot (res_slot0 + k) % stages
 };
+
+// epilogues that can take their f32 residual tile by TMA into the drained ring (EpiResLNT)
+template <class E, class = void> struct has_res_tma : std::false_type {};
+template <class E> struct has_res_tma<E, std::void_t<decltype(E::kResTma)>> : std::true_type {};
 
 // named barrier among the epilogue warps only
 __device__ __forceinline__ void epi_bar_sync(int nthreads) {
@@ -179,6 +187,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         load_a(s, kb);
         tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[s]);
       }
+      if constexpr (has_res_tma<Epi>::value && !MCAST && CLUSTER > 1) {
+        if (ep.tma_res) {   // the f32 residual tile into the next A slots as the MMAs drain them
+          static_assert(GEMM_BM * 128 == 128 * 32 * 4, "one 32-column f32 box per A slot");
+          uint64_t* rb = Epi::template res_bar<BN>(smem + Lay::EPI_OFF_ALIGNED);
+          mbar_expect_tx(rb, (BN / 32) * Lay::A_BYTES);
+          for (int k = 0; k < BN / 32; ++k) {
+            const int kb = nk + k, s = kb % STAGES;
+            mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+            tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &ep.map_res, n0 + 32 * k, m0, rb);
+          }
+        }
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -220,6 +240,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     // sub-phase stamps of CTA b < 512 go to the unused CTA slots 512 + b (tools/ln_phases.py)
     if (stamps && cta < 512 && ep_tid == 0) c.sub = stamps + size_t(512 + cta) * GEMM_STAMPS;
     c.stage = smem + Lay::A_OFF;   // every MMA has completed (tmem_full): the ring is free
+    c.ring = smem + Lay::A_OFF;
+    c.res_slot0 = nk % STAGES;
+    c.stages = STAGES;
     Epi::template run<BN, CLUSTER, NE>(ep, c, epi_smem);
     if (stamp && ep_tid == 0) stamp[5] = globaltimer();
   }
@@ -624,6 +647,14 @@ struct ResLNParams {
   X2 k = x2_consts();             // opaque FFMA2 constants (paired INT8 path, numerics.cuh)
   int tma_store = 0;              // I8_ONLY register path: the code tile leaves by one TMA store
   CUtensorMap out_map;            // ... over out_i8 [rows][hidden], box BN x 128, no swizzle
+  // small-batch f32/f16 outputs (FP layers) by TMA: bit 0 out_f32 through map_f32 (box 32 x 128
+  // f32, 128B swizzle), bit 1 out_f16 through map_f16 (box 32 x 128 f16, 64B swizzle)
+  int tma_f = 0;
+  CUtensorMap map_f32, map_f16;
+  // small-batch f32 residual by TMA: boxes of 32 x 128 f32 (128B swizzle) loaded by the
+  // producer into the first drained ring slots after the main loop (res_f32 rows)
+  int tma_res = 0;
+  CUtensorMap map_res;
 };
 // I8_ONLY: the hot INT8 chain (int8 residual, int32 accumulator, only int8 codes out):
 // the general variant's optional outputs are compiled out, shrinking the epilogue code
@@ -640,7 +671,13 @@ struct EpiResLNT {
   // cluster exchange (CLUSTER > 1): xpart [2 reductions][4][128] floats + xbar[2] mbarriers
   template <int BN> __host__ __device__ static constexpr int xp_off() { return (RED_FLOATS + 3 * BN) * 4 + 128 * res_ld<BN>(); }
   static constexpr int XP_MAX = 8;   // cluster ranks the exchange buffer holds
-  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return xp_off<BN>() + 2 * XP_MAX * 128 * 4 + 16; }
+  template <int BN> __host__ __device__ static constexpr int smem_bytes() { return xp_off<BN>() + 2 * XP_MAX * 128 * 4 + 24; }
+  static constexpr bool kResTma = true;
+  // mbarrier of the TMA-loaded residual tile (after the two exchange barriers)
+  template <int BN>
+  __device__ static uint64_t* res_bar(uint8_t* smem) {
+    return reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * XP_MAX * 128 * 4) + 2;
+  }
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
   // before the kernel's cluster-wide start barrier: the exchange barriers exist before any
   // peer's st.async can complete on them
@@ -649,6 +686,7 @@ struct EpiResLNT {
     uint64_t* xb = reinterpret_cast<uint64_t*>(smem + xp_off<BN>() + 2 * XP_MAX * 128 * 4);
     mbar_init(&xb[0], 1);
     mbar_init(&xb[1], 1);
+    mbar_init(&xb[2], 1);
   }
   template <int BN>
   __device__ static void prefetch(const Params& p, uint8_t* smem, int m0, int n0, int M, int tid, int nt) {
@@ -822,7 +860,21 @@ struct EpiResLNT {
             }
           }
         } else {
-          residual32<BN>(p, c, rtile, rbase, c.c0 + 32 * k, res);
+          if (p.tma_res) {   // residual box k from its ring slot (128B swizzle: chunk ^ (row & 7))
+            if (k == 0) {
+              mbar_wait(res_bar<BN>(smem), 0);
+            }
+            int slot = c.res_slot0 + k;
+            slot = slot >= c.stages ? slot - c.stages : slot;
+            const uint8_t* rowp = c.ring + slot * (GEMM_BM * 128) + c.tile_row * 128;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 v = *reinterpret_cast<const float4*>(rowp + ((q ^ (c.tile_row & 7)) << 4));
+              res[4 * q] = v.x; res[4 * q + 1] = v.y; res[4 * q + 2] = v.z; res[4 * q + 3] = v.w;
+            }
+          } else {
+            residual32<BN>(p, c, rtile, rbase, c.c0 + 32 * k, res);
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const uint32_t u = r[32 * k + j];
@@ -937,7 +989,54 @@ struct EpiResLNT {
             const int col = c.c0 + 32 * k + j;
             y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[32 * k + j], mean), inv), sgam[col]), sbet[col]);
           }
-          emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+          if (p.tma_f) {
+            // stage 32 columns: f32 box k (128 B rows, 128B swizzle: chunk ^ (row & 7)) and
+            // f16 box k (64 B rows, 64B swizzle: chunk ^ ((row >> 1) & 3)); the XOR acts on
+            // addresses, so the register indices stay compile-time
+            if (p.f16_round) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
+            }
+            if (p.tma_f & 1) {
+              uint8_t* rowp = c.stage + k * (128 * 128) + c.tile_row * 128;
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                *reinterpret_cast<float4*>(rowp + ((q ^ (c.tile_row & 7)) << 4)) =
+                    make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+            }
+            if (p.tma_f & 2) {
+              uint8_t* rowp = c.stage + 3 * (128 * 128) + k * (128 * 64) + c.tile_row * 64;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t hw[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  __half2 h2 = __floats2half2_rn(y[8 * q + 2 * u], y[8 * q + 2 * u + 1]);
+                  hw[u] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+                *reinterpret_cast<uint4*>(rowp + ((q ^ ((c.tile_row >> 1) & 3)) << 4)) =
+                    make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              }
+            }
+          } else {
+            emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+          }
+        }
+      }
+    }
+    if constexpr (!I8_ONLY) {
+      if (p.tma_f) {   // three 32-column boxes of each staged output, one TMA store each
+        fence_proxy_async_smem();
+        epi_bar_sync(c.ne_threads);
+        if (c.ep_tid == 0) {
+          const int m0 = c.row - c.tile_row;
+#pragma unroll
+          for (int k = 0; k < NC / 32; ++k) {
+            if (p.tma_f & 1) tma_store_2d(&p.map_f32, c.stage + k * (128 * 128), c.n0 + c.c0 + 32 * k, m0);
+            if (p.tma_f & 2) tma_store_2d(&p.map_f16, c.stage + 3 * (128 * 128) + k * (128 * 64), c.n0 + c.c0 + 32 * k, m0);
+          }
+          bulk_commit();
+          bulk_wait_read0();
         }
       }
     }

@@ -28,8 +28,16 @@ cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap&
     case 2561: return launch_gemm<KIND_F16, 256, 3, 1, 8, EpiResLN>(a, b, M, N, kb, p, st);
     case 1281: return launch_gemm<KIND_F16, 128, 3, 1, 4, EpiResLN>(a, b, M, N, kb, p, st);
     case 641: return launch_gemm<KIND_F16, 64, 4, 1, 4, EpiResLN>(a, b, M, N, kb, p, st);
-    case 968:   // (the two-thread strided epilogue measured 0.681 -> 0.695 ms FP16 p50 here)
-      return launch_gemm<KIND_F16, 96, 6, 8, 4, EpiResLNRegs96>(a, b, M, N, kb, p, st);     // small batches
+    case 968: {   // small batches (the two-thread strided epilogue measured 0.681 -> 0.695 ms FP16 p50 here)
+      // f32 (+ f16) outputs only: staged in smem and written by TMA stores (the per-row 16-byte
+      // stores of 32 rows per warp instruction were half of this epilogue); SAMP_NO_LN_TMA_STORE=1: A/B
+      EpiResLN::Params q = p;
+      const bool plain = p.out_f32 && !p.out_i8 && !p.deq_outputs && !p.amax && !p.tap_f32;
+      if (plain && !env_flag("SAMP_NO_LN_TMA_STORE")) q.tma_f = 1 | (p.out_f16 ? 2 : 0);
+      // the f32 residual tile by TMA into the drained ring (instead of per-row global loads)
+      if (p.res_f32 && !p.res_i8 && !env_flag("SAMP_NO_LN_TMA_RES")) q.tma_res = 1;
+      return launch_gemm<KIND_F16, 96, 6, 8, 4, EpiResLNRegs96>(a, b, M, N, kb, q, st);
+    }
     case 1288: return launch_gemm<KIND_F16, 128, 5, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);
   }
   return cudaErrorInvalidValue;

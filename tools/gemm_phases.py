@@ -34,7 +34,7 @@ def main():
     arch = bench.build_model()
     eng = Engine(arch, device=0)
     L = arch.manifest.num_layers
-    codes = PrecisionPlan.prefix(args.mode, L, L).codes()
+    codes = PrecisionPlan.prefix(args.mode, L, 0 if args.mode == "FP" else L).codes()
     seq_start, att, ids, segs = bench.synthetic_batch(0, args.batch, args.seq)
     dev = torch.device("cuda", 0)
     d_ids, d_segs = torch.from_numpy(ids).to(dev), torch.from_numpy(segs).to(dev)

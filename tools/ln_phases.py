@@ -22,6 +22,8 @@ import bench  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--mode", default="FULLY_QUANT")
+    ap.add_argument("--fp16-storage", action="store_true")
     args = ap.parse_args()
     import torch
     from paper_2209_09130_b200 import _lib
@@ -29,9 +31,9 @@ def main():
     from paper_2209_09130_b200.plan import PrecisionPlan
 
     arch = bench.build_model()
-    eng = Engine(arch, device=0)
+    eng = Engine(arch, device=0, fp16_storage=args.fp16_storage)
     L = arch.manifest.num_layers
-    codes = PrecisionPlan.prefix("FULLY_QUANT", L, L).codes()
+    codes = PrecisionPlan.prefix(args.mode, L, 0 if args.mode == "FP" else L).codes()
     seq_start, att, ids, segs = bench.synthetic_batch(0, args.batch, 128)
     dev = torch.device("cuda", 0)
     d_ids, d_segs = torch.from_numpy(ids).to(dev), torch.from_numpy(segs).to(dev)
@@ -62,7 +64,7 @@ def main():
     names = names.value.decode().split("\n")[: n.value]
     agg = defaultdict(list)
     for i, name in enumerate(names):
-        if name not in ("outproj_i8", "ffn2_i8"):
+        if name not in ("outproj_i8", "ffn2_i8", "outproj_f16", "ffn2_f16"):
             continue
         st = buf[i].astype(np.int64)
         for b in range(512):

@@ -1107,6 +1107,12 @@ struct EpiResLNT {
           const uint32_t w = *reinterpret_cast<const uint32_t*>(rtile + col);
 #pragma unroll
           for (int u = 0; u < 4; ++u) res[u] = deq(int(int8_t((w >> (8 * u)) & 0xff)), p.res_scale);
+        } else if (p.tma_res) {   // box col/32 in its ring slot, 16-byte chunk (col%32)/4 ^ (row & 7)
+          int slot = c.res_slot0 + col / 32;
+          slot = slot >= c.stages ? slot - c.stages : slot;
+          const float4 v = *reinterpret_cast<const float4*>(c.ring + slot * (GEMM_BM * 128) + c.tile_row * 128 +
+                                                            ((((col & 31) >> 2) ^ (c.tile_row & 7)) << 4));
+          res[0] = v.x; res[1] = v.y; res[2] = v.z; res[3] = v.w;
         } else {
           const float4 v = *reinterpret_cast<const float4*>(p.res_f32 + rbase + c.n0 + col);
           res[0] = v.x; res[1] = v.y; res[2] = v.z; res[3] = v.w;
@@ -1119,6 +1125,7 @@ struct EpiResLNT {
         }
       }
     };
+    if (p.tma_res) mbar_wait(res_bar<BN>(smem), 0);
     if (c.half == 0) fill(std::integral_constant<int, 0>{});
     else fill(std::integral_constant<int, 4>{});
     auto half_leaf = [&](auto f) {
@@ -1202,12 +1209,38 @@ struct EpiResLNT {
 #pragma unroll
           for (int u = 0; u < 4; ++u) amx = fmaxf(amx, fabsf(y[u]));
         }
+        if (p.tma_f) {   // swizzled 32-column boxes (see run_regs): f32 16-byte, f16 8-byte pieces
+          if (p.tma_f & 1)
+            *reinterpret_cast<float4*>(c.stage + (col >> 5) * (128 * 128) + c.tile_row * 128 +
+                                       ((((col & 31) >> 2) ^ (c.tile_row & 7)) << 4)) = make_float4(y[0], y[1], y[2], y[3]);
+          if (p.tma_f & 2) {
+            __half2 h0 = __floats2half2_rn(y[0], y[1]), h1 = __floats2half2_rn(y[2], y[3]);
+            *reinterpret_cast<uint2*>(c.stage + 3 * (128 * 128) + (col >> 5) * (128 * 64) + c.tile_row * 64 +
+                                      ((((col & 31) >> 3) ^ ((c.tile_row >> 1) & 3)) << 4) + (col & 4) * 2) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+          }
+          continue;
+        }
         if (p.out_f32) *reinterpret_cast<float4*>(p.out_f32 + o) = make_float4(y[0], y[1], y[2], y[3]);
         if (p.out_f16) {
           __half2 h0 = __floats2half2_rn(y[0], y[1]), h1 = __floats2half2_rn(y[2], y[3]);
           *reinterpret_cast<uint2*>(p.out_f16 + o) =
               make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
         }
+      }
+    }
+    if (p.tma_f) {   // three 32-column boxes per staged output, one TMA store each
+      fence_proxy_async_smem();
+      epi_bar_sync(c.ne_threads);
+      if (c.ep_tid == 0) {
+        const int m0 = c.row - c.tile_row;
+#pragma unroll
+        for (int k = 0; k < BN / 32; ++k) {
+          if (p.tma_f & 1) tma_store_2d(&p.map_f32, c.stage + k * (128 * 128), c.n0 + 32 * k, m0);
+          if (p.tma_f & 2) tma_store_2d(&p.map_f16, c.stage + 3 * (128 * 128) + k * (128 * 64), c.n0 + 32 * k, m0);
+        }
+        bulk_commit();
+        bulk_wait_read0();
       }
     }
     if (p.tma_store) {   // int8-only chain: the [128][96] code tile leaves by one TMA store

@@ -36,6 +36,10 @@ cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap&
       if (plain && !env_flag("SAMP_NO_LN_TMA_STORE")) q.tma_f = 1 | (p.out_f16 ? 2 : 0);
       // the f32 residual tile by TMA into the drained ring (instead of per-row global loads)
       if (p.res_f32 && !p.res_i8 && !env_flag("SAMP_NO_LN_TMA_RES")) q.tma_res = 1;
+      // SAMP_LN96_STRIDED=1: two threads per row (run_strided, TMA residual and stores too):
+      // bit-identical, measured slower (batch-1 FP16 p50 0.651 vs 0.618 ms)
+      if (q.tma_f && q.tma_res && env_flag("SAMP_LN96_STRIDED"))
+        return launch_gemm<KIND_F16, 96, 6, 8, 8, EpiResLN>(a, b, M, N, kb, q, st);
       return launch_gemm<KIND_F16, 96, 6, 8, 4, EpiResLNRegs96>(a, b, M, N, kb, q, st);
     }
     case 1288: return launch_gemm<KIND_F16, 128, 5, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);

@@ -133,7 +133,8 @@ class Engine:
         table = self.archive.calibration
         if table is None:
             return None
-        return tuple(sorted((s, float(e.amax)) for s, e in table.entries.items()))
+        # a plain list in the dict's order (a reordered but equal table only costs a re-push)
+        return [(s, e.amax) for s, e in table.entries.items()]
 
     def _push_calibration(self) -> None:
         """Send the table's amax values to the device when they differ from what it holds."""
@@ -144,7 +145,7 @@ class Engine:
             _lib.check(self._lib.samp_clear_calibration(self._h))
             self._pushed_calibration = None
             for site, amax in state or ():
-                _lib.check(self._lib.samp_set_site_amax(self._h, site.encode(), amax))
+                _lib.check(self._lib.samp_set_site_amax(self._h, site.encode(), float(amax)))
             self._pushed_calibration = state
 
     def check_plan(self, plan: PrecisionPlan) -> CalibrationTable | None:

@@ -68,6 +68,8 @@ struct EpiCtx {
   uint8_t* stage = nullptr;            // free smem (the drained operand ring) for a TMA-stored tile
   uint8_t* ring = nullptr;             // the operand ring's A slots (TMA-loaded residual boxes)
   int res_slot0 = 0, stages = 1;       // residual box k sits in A slot (res_slot0 + k) % stages
+  const uint32_t* kpart = nullptr;     // KS2: the other K half's accumulators [128][BN] (smem)
+  uint64_t* kpart_bar = nullptr;       // ... complete when all of them landed
 };
 
 // epilogues that can take their f32 residual tile by TMA into the drained ring (EpiResLNT)
@@ -106,11 +108,18 @@ struct GemmOcc {
 // MC (CLUSTER > 1): the cluster's CTAs share the A row tile; rank r loads rows
 // [r*128/CLUSTER, (r+1)*128/CLUSTER) of every stage multicast to all ranks (map_a then has
 // 128/CLUSTER-row boxes), and each MMA commit frees the stage in every rank
-template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi, bool MC = false>
+// KS2 (small batches, LayerNorm epilogues): the K range is split over the two z-halves of a
+// (CLUSTER x 1 x 2) cluster; the z = 1 CTA pushes its accumulator tile into its z = 0
+// partner's shared memory (st.async, completing on the partner's mbarrier) and the partner
+// adds it before the epilogue — int32 adds are exact, so INT8 results are unchanged
+template <int BN, bool KS2> __host__ __device__ constexpr int ks2_bytes() { return KS2 ? 128 * BN * 4 + 64 : 0; }
+
+template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi, bool MC = false, bool KS2 = false>
 __global__ void __launch_bounds__(64 + 32 * NE, GemmOcc<BN, STAGES>::value)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             int M, int k_bytes, const __grid_constant__ typename Epi::Params ep, unsigned long long* stamps) {
-  using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
+  constexpr int EPI_BYTES = (Epi::template smem_bytes<BN>() + 127) / 128 * 128;
+  using Lay = GemmLayout<BN, STAGES, EPI_BYTES + ks2_bytes<BN, KS2>()>;
   constexpr int TMEM_COLS = tmem_cols_for(BN);
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -148,6 +157,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       mbar_init(&empty[s], MCAST ? CLUSTER : 1);
     }
     mbar_init(tmem_full, 1);
+    if constexpr (KS2) mbar_init(reinterpret_cast<uint64_t*>(epi_smem + EPI_BYTES + 128 * BN * 4), 1);
     if constexpr (CLUSTER > 1) Epi::template cluster_init<BN>(epi_smem);
     fence_barrier_init();
   }
@@ -188,7 +198,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[s]);
       }
       if constexpr (has_res_tma<Epi>::value && !MCAST && CLUSTER > 1) {
-        if (ep.tma_res) {   // the f32 residual tile into the next A slots as the MMAs drain them
+        if (ep.tma_res && (!KS2 || blockIdx.z == 0)) {   // the f32 residual tile into the next A slots as the MMAs drain them
           static_assert(GEMM_BM * 128 == 128 * 32 * 4, "one 32-column f32 box per A slot");
           uint64_t* rb = Epi::template res_bar<BN>(smem + Lay::EPI_OFF_ALIGNED);
           mbar_expect_tx(rb, (BN / 32) * Lay::A_BYTES);
@@ -228,6 +238,29 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     const int half = NE == 8 ? int(warp - GEMM_EPI_WARP0) / 4 : 0;
     const int tile_row = quarter * 32 + lane_id();
     const int c0 = half * (BN / (NE / 4));
+    if constexpr (KS2) {
+      if (blockIdx.z == 1) {   // second K half: push the accumulator tile to the z = 0 partner
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const uint32_t partner = cluster_rank() - CLUSTER;
+        const uint32_t dst = mapa_rank(epi_smem + EPI_BYTES + (tile_row * BN + c0) * 4, partner);
+        const uint32_t bar = mapa_rank(epi_smem + EPI_BYTES + 128 * BN * 4, partner);
+        const uint32_t ta = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(c0);
+#pragma unroll 1
+        for (int col = 0; col < BN / (NE / 4); col += 16) {
+          uint32_t r[16];
+          tmem_ld16(ta + col, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                         :: "r"(dst + (col + 4 * q) * 4), "r"(r[4 * q]), "r"(r[4 * q + 1]), "r"(r[4 * q + 2]),
+                            "r"(r[4 * q + 3]), "r"(bar) : "memory");
+        }
+        goto epilogue_done;
+      }
+      if (ep_tid == 0) mbar_expect_tx(reinterpret_cast<uint64_t*>(epi_smem + EPI_BYTES + 128 * BN * 4), 128 * BN * 4);
+    }
     pdl_wait();   // residual tiles / outputs belong to earlier kernels
     // idle during the main loop: stage this tile's epilogue operands in smem
     Epi::template prefetch<BN>(ep, epi_smem, m0, n0, M, ep_tid, 32 * NE);
@@ -243,9 +276,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     c.ring = smem + Lay::A_OFF;
     c.res_slot0 = nk % STAGES;
     c.stages = STAGES;
+    if constexpr (KS2) {
+      c.kpart = reinterpret_cast<const uint32_t*>(epi_smem + EPI_BYTES);
+      c.kpart_bar = reinterpret_cast<uint64_t*>(epi_smem + EPI_BYTES + 128 * BN * 4);
+    }
     Epi::template run<BN, CLUSTER, NE>(ep, c, epi_smem);
     if (stamp && ep_tid == 0) stamp[5] = globaltimer();
   }
+epilogue_done:
   // non-epilogue warps mirror the epilogue's cluster barriers
   if (warp < GEMM_EPI_WARP0) {
     for (int i = 0; i < Epi::template cluster_barriers<CLUSTER>(); ++i) cluster_sync_all();
@@ -832,6 +870,14 @@ struct EpiResLNT {
       for (int k = 0; k < NC / 32; ++k)
         tmem_ld32(c.taddr + 32 * k, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * k));
       tmem_wait_ld();
+      if (c.kpart) {   // KS2: add the other K half's accumulators (int32 exact; f32 for kind::f16)
+        mbar_wait(c.kpart_bar, 0);
+        const uint32_t* kp = c.kpart + c.tile_row * BN + c.c0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          r[j] = p.acc_is_f32 ? __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __uint_as_float(kp[j])))
+                              : uint32_t(int(r[j]) + int(kp[j]));
+      }
 #pragma unroll
       for (int k = 0; k < NC / 32; ++k) {
         float res[32];
@@ -1099,6 +1145,18 @@ struct EpiResLNT {
 #pragma unroll
       for (int k = 0; k < 3; ++k) tmem_ld32(tbase + 32 * k, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * k));
       tmem_wait_ld();
+      if (c.kpart) {   // KS2: add the other K half's accumulators (int32 exact; f32 for kind::f16)
+        mbar_wait(c.kpart_bar, 0);
+        const uint32_t* kp = c.kpart + c.tile_row * BN;
+#pragma unroll
+        for (int g = 0; g < 12; ++g)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 8 * g + JO + u;
+            r[j] = p.acc_is_f32 ? __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __uint_as_float(kp[j])))
+                                : uint32_t(int(r[j]) + int(kp[j]));
+          }
+      }
 #pragma unroll
       for (int g = 0; g < 12; ++g) {
         const int col = 8 * g + JO;
@@ -1391,20 +1449,28 @@ using EpiResLNI8 = EpiResLNT<true>;
 using EpiResLNRegs96 = EpiResLNT<false, true>;
 
 // ------------------------------------------------------------------ host launcher
-template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi, bool MC = false>
+template <int KIND, int BN, int STAGES, int CLUSTER, int NE, class Epi, bool MC = false, bool KS2 = false>
 inline cudaError_t launch_gemm(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N, int k_bytes,
                                const typename Epi::Params& p, cudaStream_t stream, int ksplit = 1) {
-  using Lay = GemmLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
-  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi, MC>;
+  constexpr int EPI_BYTES = (Epi::template smem_bytes<BN>() + 127) / 128 * 128;
+  using Lay = GemmLayout<BN, STAGES, EPI_BYTES + ks2_bytes<BN, KS2>()>;
+  auto kern = gemm_kernel<KIND, BN, STAGES, CLUSTER, NE, Epi, MC, KS2>;
   static thread_local int configured_device = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_device != dev) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
     if (e != cudaSuccess) return e;
+    if (KS2 && 2 * CLUSTER > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     configured_device = dev;
   }
   unsigned long long* stamps = g_gemm_stamps;
+  if constexpr (KS2)
+    return launch_ex_cl(kern, dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, 2), dim3(64 + 32 * NE, 1, 1), Lay::TOTAL,
+                        stream, dim3(CLUSTER, 1, 2), map_a, map_b, M, k_bytes, p, stamps);
   return launch_ex(kern, dim3(N / BN, (M + GEMM_BM - 1) / GEMM_BM, ksplit), dim3(64 + 32 * NE, 1, 1), Lay::TOTAL, stream,
                    CLUSTER, map_a, map_b, M, k_bytes, p, stamps);
 }

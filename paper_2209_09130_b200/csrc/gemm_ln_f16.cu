@@ -40,6 +40,9 @@ cudaError_t gemm_ln_f16(const Tiles& t, const CUtensorMap& a, const CUtensorMap&
       // bit-identical, measured slower (batch-1 FP16 p50 0.651 vs 0.618 ms)
       if (q.tma_f && q.tma_res && env_flag("SAMP_LN96_STRIDED"))
         return launch_gemm<KIND_F16, 96, 6, 8, 8, EpiResLN>(a, b, M, N, kb, q, st);
+      // long K (FFN2): the two K halves on 16 SMs, partial tile through DSMEM (KS2)
+      if (kb >= 4096 && env_flag("SAMP_LN_KS2"))
+        return launch_gemm<KIND_F16, 96, 4, 8, 4, EpiResLNRegs96, false, true>(a, b, M, N, kb, q, st);
       return launch_gemm<KIND_F16, 96, 6, 8, 4, EpiResLNRegs96>(a, b, M, N, kb, q, st);
     }
     case 1288: return launch_gemm<KIND_F16, 128, 5, 8, 4, EpiResLN>(a, b, M, N, kb, p, st);

@@ -60,6 +60,9 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
       if (i8_only) {   // int8-only chain: compact paired epilogue, codes out by one TMA store
         EpiResLN::Params q = p;
         q.tma_store = env_flag("SAMP_NO_LN_TMA_STORE") ? 0 : 1;
+        // long K (FFN2): the two K halves on 16 SMs, partial tile through DSMEM (KS2)
+        if (kb >= 2048 && env_flag("SAMP_LN_KS2"))
+          return launch_gemm<KIND_I8, 96, 4, 8, 8, EpiResLNI8, false, true>(a, b, M, N, kb, q, st);
         return launch_gemm<KIND_I8, 96, 6, 8, 8, EpiResLNI8>(a, b, M, N, kb, q, st);
       }
       return launch_gemm<KIND_I8, 96, 6, 8, 8, EpiResLN>(a, b, M, N, kb, p, st);

@@ -67,3 +67,23 @@ def test_tma_epilogue_variants_bit_identical(arch2, monkeypatch, mode, k, fp16, 
     for env in (("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES"), ("SAMP_LN96_STRIDED",)):
         other = _run(arch2, encs, plan, monkeypatch, env, fp16)
         np.testing.assert_array_equal(base, other, err_msg=f"{mode} batch {batch} {env}")
+
+
+@pytest.mark.parametrize("mode,k,fp16", [("FULLY_QUANT", 2, False), ("FP", 0, True)])
+@pytest.mark.parametrize("batch", [1, 5])
+def test_ffn2_k_split_cluster(arch2, monkeypatch, mode, k, fp16, batch):
+    """SAMP_LN_KS2: FFN2's two K halves on the two z-halves of a 16-CTA cluster, the partial
+    accumulator tile pushed through DSMEM.  INT8: int32 adds, bit-identical; FP16: two f32
+    partial sums (the tensor path's tolerance, test_gpu_engine.py)."""
+    encs = _encs(batch, 128 if batch == 1 else 100, 7 + batch)
+    plan = PrecisionPlan.prefix(mode, 2, k)
+    base = _run(arch2, encs, plan, monkeypatch, (), fp16)
+    monkeypatch.setenv("SAMP_LN_KS2", "1")
+    from paper_2209_09130_b200.engine import Engine
+    got = Engine(arch2, fp16_storage=fp16).run_batch(encs, plan).hidden_states.copy()
+    monkeypatch.delenv("SAMP_LN_KS2")
+    if mode == "FULLY_QUANT":
+        np.testing.assert_array_equal(got, base)
+    else:
+        rel = float(np.linalg.norm(got - base) / np.linalg.norm(base))
+        assert rel < 1e-3, rel

@@ -174,6 +174,7 @@ struct samp_engine {
   samp::Geometry geo;
   int launches = 0;
   bool capture = false;
+  bool stamp_only = false;   // samp_set_profiling(2): phase stamps without per-launch events
   std::map<std::string, std::vector<uint8_t>> stages;
   std::vector<int> h_pos;
   bool profiling = false;
@@ -484,7 +485,7 @@ static void run_kernel(samp_engine* e, const char* what, F&& fn) {
     b = take_event(e);
     SAMP_CUDA(cudaEventRecord(a, e->stream_in_use));
   }
-  const bool stamped = e->profiling && e->stamps && int(e->stamp_launches.size()) < e->stamp_cap &&
+  const bool stamped = (e->profiling || e->stamp_only) && e->stamps && int(e->stamp_launches.size()) < e->stamp_cap &&
                        std::strcmp(what, "embed") != 0 &&
                        std::strcmp(what, "head") != 0;
   if (stamped) {
@@ -1419,7 +1420,10 @@ extern "C" int samp_debug_gemm_stamps_fetch(samp_engine* e, unsigned long long* 
 extern "C" int samp_set_profiling(samp_engine* e, int on) {
   std::lock_guard<std::recursive_mutex> lock(e->mu);   // threading contract (samp_b200.h)
   return guarded([&] {
-    e->profiling = on != 0;
+    // 1: per-launch CUDA events (+ stamps); 2: stamps only, kernels launched back to back
+    // with PDL as in a normal forward (no graph) — the cross-kernel timeline (tools/timeline.py)
+    e->profiling = on == 1;
+    e->stamp_only = on == 2;
     e->prof.clear();
   });
 }
@@ -1534,7 +1538,8 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
     // ---------------- device work: replay a captured CUDA graph for this (plan, batch
     // geometry, head) when one exists; capture on the second sighting of a key (the first
     // run also configures every kernel's smem attributes outside of capture)
-    const bool graphable = e->graphs_enabled && !e->capture && !e->profiling && !e->calib_amax && !e->usage;
+    const bool graphable = e->graphs_enabled && !e->capture && !e->profiling && !e->stamp_only && !e->calib_amax &&
+                           !e->usage;
     std::string key;
     if (graphable) {
       key.assign(reinterpret_cast<const char*>(prec), L);

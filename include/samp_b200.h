@@ -193,8 +193,10 @@ int samp_debug_unary(int fn, const float* x, float* y, long n);
 /* number of kernel launches issued by the last samp_forward (for bench gpu_launches) */
 int samp_last_launch_count(samp_engine* e);
 
-/* per-kernel device timing: with profiling on, every launch is bracketed by CUDA events
- * on the engine stream; samp_profile_report syncs and writes {"kernel": [total_ms, n], ...} */
+/* per-kernel device timing: with profiling on (1), every launch is bracketed by CUDA events
+ * on the engine stream; samp_profile_report syncs and writes {"kernel": [total_ms, n], ...}.
+ * 2: in-kernel phase stamps only (samp_debug_gemm_stamps), kernels launched back to back
+ * with PDL as in a normal forward (no graph, no events): the cross-kernel timeline. */
 int samp_set_profiling(samp_engine* e, int on);
 /* GEMM phase stamps (profiling mode only): samp_debug_gemm_stamps(e, n) records, for the
  * next n GEMM launches, per CTA 8 u64 = {smid, t_start, t_first_slot_full, t_last_slot_full,

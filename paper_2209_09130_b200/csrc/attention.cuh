@@ -428,8 +428,10 @@ __device__ __forceinline__ void att_extremes32(const uint32_t (&vc)[32], int k0,
 }
 
 // 32 P codes of a register chunk -> the row's 128B-swizzled P operand at tile column `local`
+// (keys >= 128 live in the next 16 KB block of 128-key rows)
 __device__ __forceinline__ void att_p_store32(uint8_t* prow, int local, int r, const uint32_t (&wv)[8]) {
-  const int chunk0 = local >> 4;
+  prow += (local >> 7) * 16384;
+  const int chunk0 = (local & 127) >> 4;
   *reinterpret_cast<uint4*>(prow + ((chunk0 ^ (r & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   *reinterpret_cast<uint4*>(prow + (((chunk0 + 1) ^ (r & 7)) << 4)) = make_uint4(wv[4], wv[5], wv[6], wv[7]);
 }
@@ -502,13 +504,15 @@ __device__ __forceinline__ void att_expo32_exact(uint32_t (&vc)[32], uint32_t ta
 // evaluated as ONE chain handed from thread to thread through shared memory in TPR
 // barrier-separated rounds, so every add happens in numpy's order and the denominator (and
 // every P code) equals att_softmax's bit for bit.
-template <int TPR>
+// MAXCH: 32-key chunks per row the caller's tiles can have (4: S <= 128, 8: S <= 256).
+template <int TPR, int MAXCH = 4>
 __device__ __forceinline__ void att_softmax_rr(const AttnParams& p, const AttRow& w, uint32_t ta, uint8_t* pbuf,
                                                uint8_t* xbuf, uint64_t* bar_p, unsigned long long* stamp) {
-  constexpr int CPT = 4 / TPR;
+  constexpr int CPT = MAXCH / TPR;
+  static_assert(CPT * 32 <= 64, "the leaf tail switch covers 64 register values per thread");
   const X2 kx = p.k;
   const int h = w.h, r = w.r, S = w.S, att = w.att, kbeg = w.kbeg;
-  const int nch = (S + 31) >> 5;               // the row's key chunks (1..4)
+  const int nch = (S + 31) >> 5;               // the row's key chunks (1..MAXCH)
   const int c_lo = h * CPT;
   const int cnt = max(0, min(CPT, nch - c_lo)); // my chunks, warp-uniform
   const int lo = 32 * c_lo;                    // sequence-local key of my first value
@@ -611,7 +615,7 @@ __device__ __forceinline__ void att_softmax_rr(const AttnParams& p, const AttRow
   // keys of the tile outside this row's sequence (packed tiles): P = 0, chunk tc by thread tc % TPR
   const int tch = w.nkp >> 5, own0 = kbeg >> 5;
 #pragma unroll
-  for (int tc = 0; tc < 4; ++tc)
+  for (int tc = 0; tc < MAXCH; ++tc)
     if (tc < tch && (tc < own0 || tc >= own0 + nch) && tc % TPR == h) {
       const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       att_p_store32(prow, 32 * tc, r, z);
@@ -734,7 +738,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
         tma_load_2d(smem + lay.k_off + b * 64 * C::ROW_BYTES, &map_qkv, H + head * 64, krow0 + b * 64, bar_load);
         tma_load_2d(smem + lay.v_off + b * 64 * C::ROW_BYTES, &map_qkv, 2 * H + head * 64, krow0 + b * 64, bar_load);
       }
-      mbar_wait(bar_load, 0);
+      mbar_wait_park(bar_load, 0);
       tc_fence_after();
       // MMA 1: S_acc[:, n0:n0+nn] = Q . K[n0:n0+nn]^T over d = 64 (K steps of 32 bytes)
       const uint32_t qa = smem_addr(smem + lay.q_off), ka = smem_addr(smem + lay.k_off);
@@ -754,7 +758,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
       const uint32_t pa = smem_addr(smem + lay.p_off), va = smem_addr(smem + lay.v_off);
       const uint32_t idesc2 = F16 ? idesc_f16(128, 64, true) : idesc_i8(128, 64, true);
       for (int ch = 0; ch < nchunks; ++ch) {
-        mbar_wait_sleep(bar_p, ch & 1);   // the softmax passes take microseconds
+        mbar_wait_park(bar_p, ch & 1);   // the softmax passes take microseconds (parked: no issue slots)
         tc_fence_after();
         const int k_lo = ch * ATT_P_CHUNK, k_hi = min(nkp, k_lo + ATT_P_CHUNK);
         for (int key = k_lo; key < k_hi; key += C::KEY_STEP) {
@@ -775,13 +779,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnParams p
     const int r = quarter * 32 + lane_id();            // query row within the tile
     const uint32_t ta = tmem + (uint32_t(quarter * 32) << 16);
     const AttRow w = att_row<TPR>(p, seq, q0, cnt, r, h);
-    mbar_wait_sleep(bar_s, 0);            // Q/K/V loads + MMA 1 (after the PDL wait)
+    mbar_wait_park(bar_s, 0);             // Q/K/V loads + MMA 1 (after the PDL wait)
     tc_fence_after();
     const bool stamper = stamp && threadIdx.x == 32;
     if (stamper) stamp[2] = globaltimer();
     const float amx_sm = att_softmax<F16, TPR, HIST>(p, w, ta, smem + lay.p_off, smem + lay.x_off, hist_s, bar_p,
                                                      bar_pf, stamper ? stamp : nullptr);
-    mbar_wait_sleep(bar_pf, (nchunks - 1) & 1);
+    mbar_wait_park(bar_pf, (nchunks - 1) & 1);
     tc_fence_after();
     att_ctx_out<F16, TPR>(p, w, ta, size_t(krow0 + q0 + r), head, amx_sm);
   }

@@ -352,9 +352,13 @@ __device__ __forceinline__ void stage_floats_async(float* dst, const float* src,
   for (int i = tid; i < n / 4; i += nthreads) cp_async16(dst + 4 * i, src + 4 * i);
 }
 __device__ __forceinline__ void stage_floats(float* dst, const float* src, int n, int tid, int nthreads) {
+#ifdef SAMP_EXP_SCALAR_STAGE
+  for (int i = tid; i < n; i += nthreads) dst[i] = __ldg(src + i);
+#else
   stage_floats_async(dst, src, n, tid, nthreads);
   cp_async_commit();
   cp_async_wait_all();
+#endif
 }
 
 // ------------------------------------------------------------------ epilogues

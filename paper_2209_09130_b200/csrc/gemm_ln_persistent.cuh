@@ -121,13 +121,24 @@ gemm_ln_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __gri
       pdl_wait();
       for (int kb = 0; kb < pre; ++kb)
         tma_load_2d(smem + Lay::A_OFF + kb * Lay::A_BYTES, &map_a, kcol(kb), tile_m0(0), &full[kb]);
+      // counters, no per-box division (gemm_persistent.cuh)
+      int kb = pre, m0 = tile_m0(0);
+      int s = pre == STAGES ? 0 : pre;
+      uint32_t par = pre == STAGES ? 0u : 1u;
       for (int it = pre; it < total; ++it) {
-        const int j = it / nk, kb = it - j * nk;
-        const int s = it % STAGES;
-        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        if (kb == nk) {
+          kb = 0;
+          m0 += ncl * GEMM_BM;
+        }
+        mbar_wait(&empty[s], par);
         mbar_expect_tx(&full[s], Lay::A_BYTES + Lay::B_BYTES);
-        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kcol(kb), tile_m0(j), &full[s]);
+        tma_load_2d(smem + Lay::A_OFF + s * Lay::A_BYTES, &map_a, kcol(kb), m0, &full[s]);
         tma_load_2d(smem + Lay::B_OFF + s * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[s]);
+        ++kb;
+        if (++s == STAGES) {
+          s = 0;
+          par ^= 1u;
+        }
       }
     }
     __syncwarp();

@@ -143,13 +143,27 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       pdl_wait();
       const int row00 = p.seq_start[p.tile_seq[item_tile(0)]];
       for (int kb = 0; kb < pre; ++kb) tma_load_2d(smem + kb * Lay::STAGE, &map_a, kb * 128, row00, &full[kb]);
+      // per-item coordinates (two dependent global loads) once per item, not per box: the
+      // issuing thread is on the MMA's critical path each time a ring slot frees
+      int j = 0, kb = pre, head = head0, row0 = row00;
+      int s = pre == QA_STAGES ? 0 : pre;
+      uint32_t par = pre == QA_STAGES ? 0u : 1u;   // ((it / QA_STAGES) & 1) ^ 1
       for (int it = pre; it < total; ++it) {
-        const int j = it / nk, kb = it - j * nk;
-        const int s = it % QA_STAGES;
-        mbar_wait_park(&empty[s], ((it / QA_STAGES) & 1) ^ 1);
+        if (kb == nk) {
+          kb = 0;
+          ++j;
+          head = item_head(j);
+          row0 = p.seq_start[p.tile_seq[item_tile(j)]];
+        }
+        mbar_wait_park(&empty[s], par);
         mbar_expect_tx(&full[s], Lay::STAGE);
-        load_w(s, kb, item_head(j));
-        tma_load_2d(smem + s * Lay::STAGE, &map_a, kb * 128, p.seq_start[p.tile_seq[item_tile(j)]], &full[s]);
+        load_w(s, kb, head);
+        tma_load_2d(smem + s * Lay::STAGE, &map_a, kb * 128, row0, &full[s]);
+        ++kb;
+        if (++s == QA_STAGES) {
+          s = 0;
+          par ^= 1u;
+        }
       }
     }
     __syncwarp();

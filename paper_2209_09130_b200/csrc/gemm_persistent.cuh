@@ -193,12 +193,13 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         for (int i = ep_tid; i < BN / 4; i += 32 * NE) cp_async16(dst + 4 * i, src + 4 * i);
         cp_async_commit();
       }
+      // the tile's coordinates (runtime div/mod) while the accumulator is still in flight
+      const int m0 = tile_m0(j), n0 = tile_n0(j);
       if (ep_tid == 0) stamp(j, 0);
       mbar_wait(&acc_full[b], (j >> 1) & 1);
       tc_fence_after();
       if (ep_tid == 0) stamp(j, 1);
-      const int m0 = tile_m0(j);
-      EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * BN + c0), m0 + tile_row, tile_row, tile_n0(j), c0,
+      EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * BN + c0), m0 + tile_row, tile_row, n0, c0,
                BN / PARTS, part, M, ep_tid, 32 * NE};
       Epi::template run<BN, 1, NE>(ep, c, epi_smem + b * Lay::EPI_STRIDE);
       tc_fence_before();

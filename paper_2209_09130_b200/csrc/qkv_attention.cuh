@@ -177,12 +177,15 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       // soon as its accumulator is free and the ring slot has landed.  The GEMM of item j+1
       // thus runs while the epilogue drains item j and the softmax works on item j-1.
       int m1 = 0, m2 = 0, g = 0, gkb = 0, it = 0;
+      // key counts of items m1 / m2 (dependent loads), refreshed as each advances, off the
+      // path from a barrier flip to the MMA issue
+      int nk1 = tile_keys(item_tile(0)), nk2 = nk1;
       while (m2 < my) {
         bool did = false;
         if (m2 < m1 && mbar_test(p_full, m2 & 1)) {
           tc_fence_after();
           const int b = m2 & 1;
-          const int nkp = tile_keys(item_tile(m2));
+          const int nkp = nk2;
           const uint32_t pa = smem_addr(smem + Lay::P_OFF);
           const uint32_t va = smem_addr(smem + Lay::QKV_OFF + b * Lay::QKV_BYTES + 2 * 128 * 64);
           for (int key = 0; key < nkp; key += 32)
@@ -190,11 +193,12 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
                             key != 0);
           mma_commit(o_full);
           ++m2;
+          if (m2 < my) nk2 = m2 == m1 ? nk1 : tile_keys(item_tile(m2));
           did = true;
         } else if (m1 == m2 && m1 < g && mbar_test(&qkv_full[m1 & 1], (m1 >> 1) & 1)) {
           tc_fence_after();
           const int b = m1 & 1;
-          const int nkp = tile_keys(item_tile(m1));
+          const int nkp = nk1;
           const uint32_t qa = smem_addr(smem + Lay::QKV_OFF + b * Lay::QKV_BYTES);
           const uint32_t ka = qa + 128 * 64;
           const uint32_t idesc_s = idesc_i8(128, nkp);
@@ -204,6 +208,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
           mma_commit(s_full);
           if (rec(m1)) rec(m1)[12] = globaltimer();
           ++m1;
+          if (m1 < my) nk1 = tile_keys(item_tile(m1));
           did = true;
         } else if (g < my && g <= m1 &&   // GEMM(j+1) only after MMA-1(j): MMAs run in issue order,
                                             // so queued GEMM work would delay the scores the softmax waits for
@@ -250,6 +255,11 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     constexpr int CW = 64 / TPR;
     auto epilogue = [&](int jj, unsigned long long* st) {
       const int b = jj & 1;
+      // the item's rows (dependent loads) before the accumulator wait
+      const int t = item_tile(jj), head = item_head(jj);
+      const int seq = p.tile_seq[t];
+      const int row0 = p.seq_start[seq];
+      const int rows = (p.seq_start[seq + 1] - row0) * p.tile_cnt[t];
       if (st) st[0] = globaltimer();
       mbar_wait_park(acc_full, jj & 1);
       tc_fence_after();
@@ -265,10 +275,6 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(acc_empty);   // the accumulator is in registers
-      const int t = item_tile(jj), head = item_head(jj);
-      const int seq = p.tile_seq[t];
-      const int row0 = p.seq_start[seq];
-      const int rows = (p.seq_start[seq + 1] - row0) * p.tile_cnt[t];
       uint8_t* buf = smem + Lay::QKV_OFF + b * Lay::QKV_BYTES + r * 64;
       const X2 kx = p.k;
 #pragma unroll
@@ -312,6 +318,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       const int t = item_tile(jc), head = item_head(jc);
       const int seq = p.tile_seq[t];
       const AttRow w = att_row<TPR>(p, seq, 0, p.tile_cnt[t], r, h);
+      const size_t ctx_row = size_t(p.seq_start[seq] + r);
       unsigned long long* st = threadIdx.x == 32 * QA_SOFT_WARP0 && j >= 0 ? rec(j) : nullptr;
       if (j >= 0) {
         mbar_wait_park(s_full, j & 1);
@@ -326,7 +333,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       mbar_wait_park(o_full, j & 1);
       tc_fence_after();
       if (st) st[8] = globaltimer();
-      att_ctx_out<false, TPR>(p, w, tmem + QA_TMEM_O + lane_base, size_t(p.seq_start[seq] + r), head, 0.0f);
+      att_ctx_out<false, TPR>(p, w, tmem + QA_TMEM_O + lane_base, ctx_row, head, 0.0f);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0 && rec(j)) atomicMax(rec(j) + 13, globaltimer());   // last warp's ctx

@@ -147,9 +147,12 @@ struct Activations {
 
 struct Geometry {
   std::vector<int> seq_start, att_len, tile_seq, tile_q0, tile_cnt;
+  std::vector<int> rt;   // per 128-row tile m: the attention tiles [rt[2m], rt[2m+1]] holding its rows
   int nseq = 0, T = 0, ntiles = 0, max_nkp = 0, max_s = 0;
   int *d_seq_start = nullptr, *d_att_len = nullptr, *d_tile_seq = nullptr, *d_tile_q0 = nullptr, *d_tile_cnt = nullptr;
-  int cap_seq = 0, cap_tiles = 0;
+  int* d_tile_done = nullptr;   // [cap_tiles] fused-kernel (tile, head) counters (row-tile flags)
+  int* d_rt = nullptr;          // [2 * cap_rt]
+  int cap_seq = 0, cap_tiles = 0, cap_rt = 0;
 };
 
 }  // namespace samp
@@ -173,6 +176,9 @@ struct samp_engine {
   samp::Activations act;
   samp::Geometry geo;
   int launches = 0;
+  // row-tile flags between the fused QKV+attention kernel and the out-projection (per forward)
+  bool dep_on = false;
+  int dep_count = 0;   // fused layers enqueued so far: the counters' target is dep_count * heads
   bool capture = false;
   bool stamp_only = false;   // samp_set_profiling(2): phase stamps without per-launch events
   std::map<std::string, std::vector<uint8_t>> stages;
@@ -344,9 +350,33 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
   }
   g.T = seq_start[nseq];
   g.ntiles = int(g.tile_seq.size());
+  // row tiles -> attention tiles (tiles are in row order; a tile holds whole sequences, or
+  // 128 query rows of one)
+  const int mt = (g.T + GEMM_BM - 1) / GEMM_BM;
+  g.rt.assign(2 * std::max(mt, 1), 0);
+  for (int m = 0, t = 0; m < mt; ++m) {
+    const int r0 = m * GEMM_BM, r1 = std::min(g.T, r0 + GEMM_BM);
+    auto tile_rows = [&](int k, int& a, int& b) {
+      const int sq = g.tile_seq[k], S = seq_start[sq + 1] - seq_start[sq];
+      a = seq_start[sq] + g.tile_q0[k];
+      b = g.tile_cnt[k] > 1 ? seq_start[sq + g.tile_cnt[k]] : a + std::min(128, S - g.tile_q0[k]);
+    };
+    int a0, b0;
+    tile_rows(t, a0, b0);
+    while (b0 <= r0) tile_rows(++t, a0, b0);
+    int hi = t, ah, bh;
+    while (hi + 1 < g.ntiles && (tile_rows(hi + 1, ah, bh), ah < r1)) ++hi;
+    g.rt[2 * m] = t;
+    g.rt[2 * m + 1] = hi;
+  }
   // captured graphs bake these device pointers into kernel arguments: a reallocation
   // invalidates every graph
-  if (nseq + 1 > g.cap_seq || g.ntiles > g.cap_tiles) clear_graphs(e);
+  if (nseq + 1 > g.cap_seq || g.ntiles > g.cap_tiles || mt > g.cap_rt) clear_graphs(e);
+  if (mt > g.cap_rt) {
+    if (g.d_rt) e->mem.release(g.d_rt);
+    g.cap_rt = std::max(mt, 64);
+    g.d_rt = e->mem.alloc<int>(2 * g.cap_rt);
+  }
   if (nseq + 1 > g.cap_seq) {
     if (g.d_seq_start) { e->mem.release(g.d_seq_start); e->mem.release(g.d_att_len); }
     g.cap_seq = std::max(nseq + 1, 64);
@@ -354,11 +384,15 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
     g.d_att_len = e->mem.alloc<int>(g.cap_seq);
   }
   if (g.ntiles > g.cap_tiles) {
-    if (g.d_tile_seq) { e->mem.release(g.d_tile_seq); e->mem.release(g.d_tile_q0); e->mem.release(g.d_tile_cnt); }
+    if (g.d_tile_seq) {
+      e->mem.release(g.d_tile_seq); e->mem.release(g.d_tile_q0); e->mem.release(g.d_tile_cnt);
+      e->mem.release(g.d_tile_done);
+    }
     g.cap_tiles = std::max(g.ntiles, 64);
     g.d_tile_seq = e->mem.alloc<int>(g.cap_tiles);
     g.d_tile_q0 = e->mem.alloc<int>(g.cap_tiles);
     g.d_tile_cnt = e->mem.alloc<int>(g.cap_tiles);
+    g.d_tile_done = e->mem.alloc<int>(g.cap_tiles);
   }
   ensure_activations(e, g.T);
   SAMP_CUDA(cudaMemcpyAsync(g.d_seq_start, g.seq_start.data(), (nseq + 1) * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
@@ -366,6 +400,7 @@ static void set_geometry(samp_engine* e, int nseq, const int32_t* seq_start, con
   SAMP_CUDA(cudaMemcpyAsync(g.d_tile_seq, g.tile_seq.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(g.d_tile_q0, g.tile_q0.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(g.d_tile_cnt, g.tile_cnt.data(), g.ntiles * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
+  SAMP_CUDA(cudaMemcpyAsync(g.d_rt, g.rt.data(), 2 * mt * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaMemcpyAsync(e->act.pos, e->h_pos.data(), g.T * sizeof(int), cudaMemcpyHostToDevice, e->stream_in_use));
   SAMP_CUDA(cudaStreamSynchronize(e->stream_in_use));  // host vectors may change on the next call
 }
@@ -566,6 +601,15 @@ static int splitk_factor(int T, int N, int kblocks, int sms) {
     if (kblocks % d == 0 && tiles * d <= sms + sms / 4) best = d;
   return best;
 }
+// the out-projection launch gemm_ln_i8 picks reads its A rows by the row-tile flags (one tile
+// per CTA, no A multicast); the persistent and split-K variants wait for the whole grid
+static bool outproj_dep_ok(samp_engine* e) {
+  const int T = e->geo.T, H = e->d.hidden, mtiles = (T + GEMM_BM - 1) / GEMM_BM;
+  if (mtiles >= 256 || env_flag("SAMP_LN_PERSISTENT") || env_flag("SAMP_LN_MCAST")) return false;
+  if (ln_rows_supported(H) && H % 64 == 0 && splitk_factor(T, H, H / 128, e->sms) >= 2) return false;
+  return true;
+}
+
 static bool ln_gemm_splitk(samp_engine* e, const char* name, const CUtensorMap& a_map, const CUtensorMap& b64,
                            int K, const EpiResLN::Params& lp, cudaStream_t st) {
   const int T = e->geo.T, H = e->d.hidden;
@@ -769,6 +813,11 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       fq.qkv_out = e->capture ? a.qkv_i8 : nullptr;
       fq.heads = e->d.num_heads;
       fq.ntiles = e->geo.ntiles;
+      if (e->dep_on) {
+        fq.tile_done = e->geo.d_tile_done;
+        fq.late_trigger = env_flag("SAMP_QA_LATE_TRIGGER");
+        ++e->dep_count;
+      }
       check_launch(e, launch_qkv_attention(a.a_xq[cur], w.m_qkv_i8_64, fq, e->sms, st), "qkv_attention_i8");
       record(e, "qkv_q", i, a.qkv_i8, size_t(T) * 3 * H);
     } else {
@@ -805,6 +854,11 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
       lp.out_f16 = a.ln1_f16;
     }
     if (e->taps) lp.tap_f32 = e->tap_ln;
+    if (fused && e->dep_on) {
+      lp.dep_cnt = e->geo.d_tile_done;
+      lp.dep_rt = e->geo.d_rt;
+      lp.dep_target = e->dep_count * e->d.num_heads * 4 * qa_tpr();
+    }
     if (!ln_gemm_splitk(e, "outproj_i8", a.a_ctx_i8, w.m_wo_i8_64, H, lp, st))
       check_launch(e, gemm_ln_i8(tln, a.a_ctx_i8, ln_small ? w.m_wo_i8_s : w.m_wo_i8, T, H, H, lp, st, a.a_ctx_i8_mc), "outproj_i8");
     tap_record(e, lsite(i, "ffn", "in"), e->tap_ln, size_t(T) * H * 4);
@@ -962,6 +1016,14 @@ static void enqueue_kernels(samp_engine* e, const uint8_t* prec, int nseq, int h
   const int L = d.num_layers, H = d.hidden, T = e->geo.T;
   Activations& a = e->act;
   const bool first_int8 = prec[0] == SAMP_LAYER_FULL_INT8 || prec[0] == SAMP_LAYER_MHA_INT8;
+  // SAMP_QA_FLAGS=1 (opt-in, measured slower): the out-projection of a fused layer starts on
+  // row tiles the fused kernel has published instead of waiting for the whole grid (off in
+  // the capture / tap / usage modes, exact mode, and when launches are dropped for measurement)
+  e->dep_count = 0;
+  e->dep_on = !e->exact && !e->taps && !e->usage && !e->capture && e->geo.max_nkp <= 128 && H % 128 == 0 &&
+              !env_flag("SAMP_NO_QA_FUSED") && env_flag("SAMP_QA_FLAGS") && !std::getenv("SAMP_SKIP") &&
+              outproj_dep_ok(e);
+  if (e->dep_on) SAMP_CUDA(cudaMemsetAsync(e->geo.d_tile_done, 0, e->geo.ntiles * sizeof(int), st));
   EmbedParams ep{};
   ep.ids = a.ids;
   ep.segs = a.segs;

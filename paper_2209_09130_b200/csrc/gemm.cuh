@@ -75,6 +75,14 @@ struct EpiCtx {
 // epilogues that can take their f32 residual tile by TMA into the drained ring (EpiResLNT)
 template <class E, class = void> struct has_res_tma : std::false_type {};
 template <class E> struct has_res_tma<E, std::void_t<decltype(E::kResTma)>> : std::true_type {};
+// epilogues whose Params carry row-tile flags (ResLNParams)
+template <class E, class = void> struct has_dep : std::false_type {};
+template <class E> struct has_dep<E, std::void_t<decltype(std::declval<typename E::Params>().dep_cnt)>> : std::true_type {};
+template <class Epi>
+__device__ __forceinline__ bool dep_set(const typename Epi::Params& ep) {
+  if constexpr (has_dep<Epi>::value) return ep.dep_cnt != nullptr;
+  else return false;
+}
 
 // named barrier among the epilogue warps only
 __device__ __forceinline__ void epi_bar_sync(int nthreads) {
@@ -88,11 +96,6 @@ __device__ __forceinline__ void epi_bar_sync(int nthreads) {
 constexpr int GEMM_STAMPS = 8, GEMM_STAMP_CTAS = 1024;
 inline unsigned long long* g_gemm_stamps = nullptr;
 
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -188,7 +191,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         mbar_expect_tx(&full[kb], Lay::A_BYTES + Lay::B_BYTES);
         tma_load_2d(smem + Lay::B_OFF + kb * Lay::B_BYTES, &map_b, kcol(kb), n0, &full[kb]);
       }
-      pdl_wait();
+      if constexpr (has_dep<Epi>::value) {
+        if (ep.dep_cnt) {
+          const int m = m0 / GEMM_BM;
+          wait_tile_flags(ep.dep_cnt, ep.dep_rt[2 * m], ep.dep_rt[2 * m + 1], ep.dep_target);
+        } else {
+          pdl_wait();
+        }
+      } else {
+        pdl_wait();
+      }
       for (int kb = 0; kb < pre; ++kb) load_a(kb, kb);
       for (int kb = pre; kb < nk; ++kb) {
         const int s = kb % STAGES;
@@ -261,7 +273,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       }
       if (ep_tid == 0) mbar_expect_tx(reinterpret_cast<uint64_t*>(epi_smem + EPI_BYTES + 128 * BN * 4), 128 * BN * 4);
     }
-    pdl_wait();   // residual tiles / outputs belong to earlier kernels
+    if (!dep_set<Epi>(ep)) pdl_wait();   // residual tiles / outputs belong to earlier kernels
     // idle during the main loop: stage this tile's epilogue operands in smem
     Epi::template prefetch<BN>(ep, epi_smem, m0, n0, M, ep_tid, 32 * NE);
     epi_bar_sync(32 * NE);
@@ -697,6 +709,13 @@ struct ResLNParams {
   // producer into the first drained ring slots after the main loop (res_f32 rows)
   int tma_res = 0;
   CUtensorMap map_res;
+  // row-tile flags (sm100.cuh): with dep_cnt set, the A rows of row tile m are read once
+  // dep_cnt[t] >= dep_target for the producer tiles t in [dep_rt[2m], dep_rt[2m+1]], and the
+  // kernel does not wait for its predecessor grid (it only reads the predecessor's A rows;
+  // its other inputs are older, its outputs not read by a grid still running)
+  const int* dep_cnt = nullptr;
+  const int* dep_rt = nullptr;
+  int dep_target = 0;
 };
 // I8_ONLY: the hot INT8 chain (int8 residual, int32 accumulator, only int8 codes out):
 // the general variant's optional outputs are compiled out, shrinking the epilogue code

@@ -52,6 +52,7 @@ cudaError_t launch_attention_i8(const CUtensorMap& map, const AttnParams& p, int
 cudaError_t launch_attention_f16(const CUtensorMap& map, const AttnParams& p, int ntiles, int heads, int keys_cap,
                                  cudaStream_t st);
 // qkv_attention.cu: fused INT8 QKV GEMM + attention (every tile S <= 128, H % 128 == 0)
+int qa_tpr();   // threads per query row of the fused kernel (SAMP_QA_TPR=2: 2, else 4)
 cudaError_t launch_qkv_attention(const CUtensorMap& a, const CUtensorMap& w64, const QAParams& q, int sms,
                                  cudaStream_t st);
 // misc_kernels.cu

@@ -25,10 +25,14 @@ static cudaError_t launch_qa_tpr(const CUtensorMap& a, const CUtensorMap& w, con
   return launch_ex(qkv_attention_kernel<TPR>, dim3(grid), dim3(qa_threads<TPR>()), QALayout::TOTAL, st, 1, a, w, qq);
 }
 
+int qa_tpr() {
+  const char* f = std::getenv("SAMP_QA_TPR");
+  return f && std::atoi(f) == 2 ? 2 : 4;
+}
+
 cudaError_t launch_qkv_attention(const CUtensorMap& a, const CUtensorMap& w64, const QAParams& q, int sms,
                                  cudaStream_t st) {
-  const char* f = std::getenv("SAMP_QA_TPR");
-  if (f && std::atoi(f) == 2) return launch_qa_tpr<2>(a, w64, q, sms, st);
+  if (qa_tpr() == 2) return launch_qa_tpr<2>(a, w64, q, sms, st);
   return launch_qa_tpr<4>(a, w64, q, sms, st);
 }
 

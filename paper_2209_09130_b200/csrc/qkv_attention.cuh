@@ -60,6 +60,11 @@ struct QAParams {
   float sout0, sout1, sout2;   // F32(scale(L.attn.{q,k,v}))
   int8_t* qkv_out;         // optional [T][3H]: also store the q|k|v codes (stage capture)
   int heads, ntiles;
+  // optional [ntiles] counters: +1 per softmax warp of a finished (tile, head) item once its
+  // ctx rows are stored (release; 4 * TPR per item); the out-projection then starts on finished row tiles instead of
+  // waiting for the whole grid, and this kernel triggers its dependents at its start
+  int* tile_done;
+  int late_trigger;        // measurement: keep the end-of-MMA trigger with tile_done set
 };
 
 template <int TPR>
@@ -250,6 +255,9 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     for (int i = tid; i < 3 * H; i += 128 * TPR) sbias[i] = __ldg(q.bias + i);   // weights: before the PDL wait
     att_bar<TPR>();
     pdl_wait();   // ctx rows (and the capture copy) belong to the activation buffers of earlier kernels
+    // every CTA of this persistent grid is resident: the out-projection's CTAs may launch
+    // onto SMs as ours exit and start on the row tiles already published in tile_done
+    if (q.tile_done && !q.late_trigger && tid == 0) pdl_trigger();
     // QKV epilogue of item jj: thread h converts columns [h*CW, h*CW + CW) of each of q, k, v
     // (EpiQKV's arithmetic on FFMA2 pairs: same roundings, gemm.cuh)
     constexpr int CW = 64 / TPR;
@@ -334,6 +342,10 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       tc_fence_after();
       if (st) st[8] = globaltimer();
       att_ctx_out<false, TPR>(p, w, tmem + QA_TMEM_O + lane_base, ctx_row, head, 0.0f);
+      if (q.tile_done) {   // publish: the warp's ctx stores, then one release add per warp
+        __syncwarp();
+        if (lane_id() == 0) red_release_gpu_add(q.tile_done + t, 1);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0 && rec(j)) atomicMax(rec(j) + 13, globaltimer());   // last warp's ctx

@@ -130,6 +130,42 @@ __device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ------------------------------------------------------------------ cross-grid row-tile flags
+// A producer grid publishes finished row tiles (counter += 1 per finished piece, release at
+// GPU scope after a CTA barrier, the CUTLASS semaphore pattern); a consumer grid launched
+// early (PDL trigger at the producer's start) acquires the counters of the tiles it reads
+// instead of waiting for the whole producer grid (griddepcontrol.wait).  The consumer reads
+// the tiles by TMA (async proxy): proxy fence after the acquire.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// spin until cnt[t] >= target for t in [lo, hi]; a flag that never arrives (a producer that
+// was not launched) traps after ~2 s instead of hanging the GPU
+__device__ __forceinline__ void wait_tile_flags(const int* cnt, int lo, int hi, int target) {
+  const unsigned long long t0 = globaltimer();
+  for (int t = lo; t <= hi; ++t) {
+    while (ld_acquire_gpu(cnt + t) < target) {
+      __nanosleep(64);
+      if (globaltimer() - t0 > 2000000000ull) __trap();
+    }
+  }
+  fence_proxy_async_global();
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(map)) : "memory");

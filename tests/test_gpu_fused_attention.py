@@ -54,14 +54,20 @@ def _engine(arch):
     return Engine(arch)
 
 
-def _run(arch, encs, plan, monkeypatch, fused):
+def _run(arch, encs, plan, monkeypatch, fused, env=()):
     if fused:
         monkeypatch.delenv("SAMP_NO_QA_FUSED", raising=False)
     else:
         monkeypatch.setenv("SAMP_NO_QA_FUSED", "1")
+    for k in env:
+        monkeypatch.setenv(k, "1")
     eng = _engine(arch)   # fresh engine: no captured graph of the other path
     out = eng.run_batch(encs, plan).hidden_states.copy()
-    monkeypatch.delenv("SAMP_NO_QA_FUSED", raising=False)
+    eng.run_batch(encs, plan)   # graph replay (the counters are reset inside the graph)
+    again = eng.run_batch(encs, plan).hidden_states.copy()
+    np.testing.assert_array_equal(out, again)
+    for k in ("SAMP_NO_QA_FUSED",) + tuple(env):
+        monkeypatch.delenv(k, raising=False)
     return out
 
 
@@ -132,6 +138,23 @@ def test_fused_equals_unfused(base2, monkeypatch, specs):
     fused = _run(arch, encs, plan, monkeypatch, True)
     ref = _run(arch, encs, plan, monkeypatch, False)
     np.testing.assert_array_equal(fused, ref)
+
+
+@pytest.mark.parametrize("specs", [
+    [(128, 128)] * 32,
+    MIXED * 6,                                           # row tiles straddling packed / ragged tiles
+    [(100, 100)] * 40 + [(64, 64)] * 7,                  # no row tile aligned with a sequence
+    [(128, 128)],
+], ids=["c2", "mixed", "ragged", "batch1"])
+def test_row_tile_flags_equal_grid_wait(base2, monkeypatch, specs):
+    """The out-projection reading its ctx rows by the fused kernel's per-tile counters
+    (SAMP_QA_FLAGS=1, opt-in) equals waiting for the whole fused grid (default), bit for bit."""
+    arch, _ = base2
+    encs = _batch(np.random.default_rng(3 + len(specs)), specs)
+    plan = PrecisionPlan.prefix("FULLY_QUANT", 2, 2)
+    flags = _run(arch, encs, plan, monkeypatch, True, env=("SAMP_QA_FLAGS",))
+    grid = _run(arch, encs, plan, monkeypatch, True)
+    np.testing.assert_array_equal(flags, grid)
 
 
 def test_fused_bert_large_geometry(monkeypatch):

@@ -68,6 +68,8 @@ struct EpiCtx {
   uint8_t* stage = nullptr;            // free smem (the drained operand ring) for a TMA-stored tile
   uint8_t* ring = nullptr;             // the operand ring's A slots (TMA-loaded residual boxes)
   int res_slot0 = 0, stages = 1;       // residual box k sits in A slot (res_slot0 + k) % stages
+  const uint8_t* table = nullptr;      // persistent kernels: the shared read-only table (GELU
+                                       // tanh); smem then holds only the tile's bias
   const uint32_t* kpart = nullptr;     // KS2: the other K half's accumulators [128][BN] (smem)
   uint64_t* kpart_bar = nullptr;       // ... complete when all of them landed
 };
@@ -509,6 +511,7 @@ struct EpiGeluQuantT {
   static constexpr bool kStagedBias = !SAMP_BIAS_GLOBAL;
   using Params = GeluQuantParams;
   template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
+  static constexpr int kTableBytes = sizeof(TanhTable);   // read-only: shared by persistent buffers
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
   template <int BN>
   __device__ static void prefetch(const Params& p, uint8_t* smem, int, int n0, int, int tid, int nt) {
@@ -530,8 +533,8 @@ struct EpiGeluQuantT {
   }
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
-    const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
-    const float* sbias = reinterpret_cast<const float*>(smem + sizeof(TanhTable));
+    const TanhTable* tt = reinterpret_cast<const TanhTable*>(c.table ? c.table : smem);
+    const float* sbias = reinterpret_cast<const float*>(c.table ? smem : smem + sizeof(TanhTable));
     const Recip rq = make_recip(p.s_out);
     // CH columns per TMEM load: 16 keeps the one-tile kernel under its 96-register cap
 #ifndef SAMP_GELU_CHUNK
@@ -630,6 +633,7 @@ struct EpiF16Out {
     int block_cols;       // columns per site (QKV: H -> q|k|v sites); 0 = one site
   };
   template <int BN> __host__ __device__ static constexpr int smem_bytes() { return sizeof(TanhTable) + BN * 4; }
+  static constexpr int kTableBytes = sizeof(TanhTable);   // read-only: shared by persistent buffers
   template <int CLUSTER> __device__ static constexpr int cluster_barriers() { return 0; }
   template <int BN>
   __device__ static void prefetch(const Params& p, uint8_t* smem, int, int n0, int, int tid, int nt) {
@@ -638,8 +642,8 @@ struct EpiF16Out {
   }
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
-    const TanhTable* tt = reinterpret_cast<const TanhTable*>(smem);
-    const float* sbias = reinterpret_cast<const float*>(smem + sizeof(TanhTable));
+    const TanhTable* tt = reinterpret_cast<const TanhTable*>(c.table ? c.table : smem);
+    const float* sbias = reinterpret_cast<const float*>(c.table ? smem : smem + sizeof(TanhTable));
     float amx = 0.0f;
 #pragma unroll 1
     for (int col = 0; col < c.ncols; col += 32) {

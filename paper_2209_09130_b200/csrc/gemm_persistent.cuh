@@ -25,17 +25,28 @@
 namespace samp {
 
 
-template <int BN, int STAGES, int EPI_BYTES>
+// epilogues with a read-only table (the GELU tanh table, 8 KB): one copy shared by both
+// epilogue buffers instead of one per buffer (two copies pushed the 128-wide FFN1 ring past
+// half of the SM's shared memory: one CTA per SM, the persistent grid ran as two waves)
+template <class E, class = void> struct epi_table_bytes { static constexpr int value = 0; };
+template <class E> struct epi_table_bytes<E, std::void_t<decltype(E::kTableBytes)>> {
+  static constexpr int value = E::kTableBytes;
+};
+
+template <int BN, int STAGES, int EPI_BYTES, int TABLE_BYTES = 0>
 struct PersistLayout {
   static constexpr int A_BYTES = GEMM_BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = STAGES * A_BYTES;
   static constexpr int BAR_OFF = B_OFF + STAGES * B_BYTES;             // full, empty, acc_full[2], acc_empty[2]
-  static constexpr int EPI_STRIDE = (EPI_BYTES + 127) & ~127;
-  static constexpr int EPI_OFF = (BAR_OFF + 8 * (2 * STAGES + 4) + 8 + 127) & ~127;
+  static constexpr int EPI_STRIDE = (EPI_BYTES - TABLE_BYTES + 127) & ~127;   // per-buffer part
+  static constexpr int TBL_OFF = (BAR_OFF + 8 * (2 * STAGES + 4) + 8 + 127) & ~127;
+  static constexpr int EPI_OFF = TBL_OFF + ((TABLE_BYTES + 127) & ~127);
   static constexpr int TOTAL = EPI_OFF + 2 * EPI_STRIDE + 1024;
 };
+template <int BN, int STAGES, class Epi>
+using PersistLayoutFor = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>(), epi_table_bytes<Epi>::value>;
 
 // CTAS: persistent CTAs per SM (2 for the epilogue-bound FFN1: two CTAs' epilogue warps
 // hide each other's MUFU / TMEM latencies; measured 24.2 vs 26.5 us at 4096 tokens)
@@ -44,10 +55,11 @@ __global__ void __launch_bounds__(64 + 32 * NE, CTAS)
 gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        int M, int N, int k_bytes, const typename Epi::Params ep, unsigned long long* stamps,
                        int n_fastest) {
-  using Lay = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
+  using Lay = PersistLayoutFor<BN, STAGES, Epi>;
+  constexpr int TBL = epi_table_bytes<Epi>::value;
   constexpr int TMEM_COLS = tmem_cols_for(2 * BN);
   constexpr int PARTS = NE / 4;
-  constexpr int EPI_BIAS_OFF = Epi::template smem_bytes<BN>() - BN * 4;
+  constexpr int EPI_BIAS_OFF = Epi::template smem_bytes<BN>() - TBL - BN * 4;   // within a buffer
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(2 * BN <= 512 && BN % 16 == 0, "two accumulators must fit TMEM");
   static_assert(NE == 8 || NE == 16, "epilogue warps");
@@ -181,8 +193,17 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
     const int c0 = part * (BN / PARTS);
     pdl_wait();
     // both buffers: read-only tables + the first two tiles' bias
-    for (int b = 0; b < 2 && b < my_tiles; ++b)
-      Epi::template prefetch<BN>(ep, epi_smem + b * Lay::EPI_STRIDE, tile_m0(b), tile_n0(b), M, ep_tid, 32 * NE);
+    if constexpr (TBL > 0) {   // the shared table once, each buffer its tile's bias
+      load_tanh_table(reinterpret_cast<TanhTable*>(smem + Lay::TBL_OFF), ep_tid, 32 * NE);
+      for (int b = 0; b < 2 && b < my_tiles; ++b)
+        stage_floats_async(reinterpret_cast<float*>(epi_smem + b * Lay::EPI_STRIDE), ep.bias + tile_n0(b), BN, ep_tid,
+                           32 * NE);
+      cp_async_commit();
+      cp_async_wait_all();
+    } else {
+      for (int b = 0; b < 2 && b < my_tiles; ++b)
+        Epi::template prefetch<BN>(ep, epi_smem + b * Lay::EPI_STRIDE, tile_m0(b), tile_n0(b), M, ep_tid, 32 * NE);
+    }
     epi_bar_sync(32 * NE);
     for (int j = 0; j < my_tiles; ++j) {
       const int b = j & 1;
@@ -201,6 +222,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
       if (ep_tid == 0) stamp(j, 1);
       EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * BN + c0), m0 + tile_row, tile_row, n0, c0,
                BN / PARTS, part, M, ep_tid, 32 * NE};
+      if constexpr (TBL > 0) c.table = smem + Lay::TBL_OFF;
       Epi::template run<BN, 1, NE>(ep, c, epi_smem + b * Lay::EPI_STRIDE);
       tc_fence_before();
       __syncwarp();
@@ -234,18 +256,31 @@ inline int device_sm_count() {
 template <int KIND, int BN, int STAGES, int NE, class Epi, int CTAS = 1>
 inline cudaError_t launch_gemm_persistent(const CUtensorMap& map_a, const CUtensorMap& map_b, int M, int N,
                                           int k_bytes, const typename Epi::Params& p, cudaStream_t stream) {
-  using Lay = PersistLayout<BN, STAGES, Epi::template smem_bytes<BN>()>;
+  using Lay = PersistLayoutFor<BN, STAGES, Epi>;
   auto kern = gemm_persistent_kernel<KIND, BN, STAGES, NE, Epi, CTAS>;
-  static thread_local int configured = -1;
+  static thread_local int configured = -1, resident = CTAS;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured != dev) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
     if (e != cudaSuccess) return e;
+    max_carveout_once(kern);
+    // the grid must be resident at once (a persistent grid larger than the SMs can hold runs
+    // as two waves: the 128-wide FFN1 did at 116.9 KB per CTA before its GELU table was
+    // shared).  Shared memory is the binding limit here; the occupancy API reports one CTA
+    // per SM even where two demonstrably co-reside (tools/ubench/occ_probe.cu), so count it.
+    int per_sm = 0, reserved = 0;
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    const int fit = per_sm / (Lay::TOTAL + reserved);
+    resident = fit < 1 ? 1 : fit < CTAS ? fit : CTAS;
     configured = dev;
+    if (std::getenv("SAMP_DEBUG_OCC"))
+      std::fprintf(stderr, "[persistent] BN %d stages %d NE %d CTAS %d smem %d -> %d resident per SM\n", BN, STAGES,
+                   NE, CTAS, Lay::TOTAL, resident);
   }
   const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * (N / BN);
-  const int slots = device_sm_count() * CTAS;
+  const int slots = device_sm_count() * resident;
   const int grid = tiles < slots ? tiles : slots;
   unsigned long long* stamps = g_gemm_stamps;
   // activations past ~48 MB (C5: 262k tokens) would be streamed from HBM once per weight

@@ -4,6 +4,7 @@
 // "shared memory descriptor" and "instruction descriptor" tables.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 #include <cuda.h>

@@ -1,6 +1,6 @@
 """Per-tile phase timeline of the persistent GEMMs (FFN1) from in-kernel stamps.
 
-    python tools/persist_phases.py [--batch 32]
+    python tools/persist_phases.py [--batch 32] [--workload c4] [--name ffn1_i8]
 
 For the first FFN1 launch of a FULLY_QUANT forward prints, per CTA (first 64), the tile
 count and, averaged over its tiles: epilogue wait for the accumulator, epilogue run time,
@@ -23,25 +23,41 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--name", default="ffn1_i8")
+    ap.add_argument("--workload", default=None, help="a bench.py workload (its model and batch)")
     args = ap.parse_args()
     import torch
     from paper_2209_09130_b200 import _lib
-    from paper_2209_09130_b200.engine import HEAD_CLASSIFY, IO_DEVICE, Engine
+    from paper_2209_09130_b200.engine import HEAD_CLASSIFY, HEAD_TAG, IO_DEVICE, Engine
     from paper_2209_09130_b200.plan import PrecisionPlan
 
-    arch = bench.build_model()
+    wl = bench.WORKLOADS[args.workload] if args.workload else None
+    arch = bench.build_model(wl) if wl else bench.build_model()
     eng = Engine(arch, device=0)
     L = arch.manifest.num_layers
+    if arch.calibration is None:   # as bench.py: on-device calibration of the synthetic model
+        from paper_2209_09130_b200.tokenization import EncodedInput
+        c_start, _, c_ids, c_segs = bench.synthetic_batch(1, 8, wl.seq, wl.pairs)
+        arch.calibration = eng.calibrate([EncodedInput(c_ids[c_start[i]:c_start[i + 1]].tolist(),
+                                                       c_segs[c_start[i]:c_start[i + 1]].tolist(), wl.seq)
+                                          for i in range(8)])
+        eng._push_calibration()
     codes = PrecisionPlan.prefix("FULLY_QUANT", L, L).codes()
-    seq_start, att, ids, segs = bench.synthetic_batch(0, args.batch, bench.SEQ)
+    if wl:
+        seq_start, att, ids, segs = bench.workload_batch(wl, 0, 1)
+        args.batch = len(att)
+    else:
+        seq_start, att, ids, segs = bench.synthetic_batch(0, args.batch, bench.SEQ)
+    tag = wl is not None and wl.task == "sequence_labeling"
     dev = torch.device("cuda", 0)
     d_ids, d_segs = torch.from_numpy(ids).to(dev), torch.from_numpy(segs).to(dev)
     nl = arch.manifest.num_labels
-    d_logits = torch.empty((args.batch, nl), dtype=torch.float32, device=dev)
+    rows = int(seq_start[-1]) if tag else args.batch
+    d_logits = torch.empty((rows, nl), dtype=torch.float32, device=dev)
     d_probs = torch.empty_like(d_logits)
-    d_labels = torch.empty(args.batch, dtype=torch.int32, device=dev)
+    d_labels = torch.empty(rows, dtype=torch.int32, device=dev)
     lib = _lib.load()
-    out = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(), HEAD_CLASSIFY)
+    out = _lib.Outputs(None, d_logits.data_ptr(), d_probs.data_ptr(), d_labels.data_ptr(),
+                       HEAD_TAG if tag else HEAD_CLASSIFY)
 
     def fwd():
         _lib.check(lib.samp_forward(eng.handle, codes, args.batch, seq_start.ctypes.data, att.ctypes.data,

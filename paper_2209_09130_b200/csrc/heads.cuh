@@ -199,16 +199,42 @@ static __global__ void __launch_bounds__(HEAD_THREADS) classifier_kernel(const H
   }
 }
 
-// one warp per token
+// one warp per token; the token's row is loaded into registers once (all of its loads in
+// flight together) and reused for every label: the same per-lane FMA order as warp_dot
+constexpr int TAG_MAX_V = 8;   // float4 per lane: H <= 1024
 static __global__ void __launch_bounds__(HEAD_THREADS) tag_kernel(const HeadParams p) {
   pdl_trigger();
   pdl_wait();
   const int H = p.hidden_size, L = p.num_labels;
   const int t = blockIdx.x * (HEAD_THREADS / 32) + threadIdx.x / 32;
   if (t >= p.T) return;
+  const int lane = threadIdx.x % 32;
   const float* h = p.hidden + size_t(t) * H;
+  float4 hv[TAG_MAX_V];
+#pragma unroll
+  for (int i = 0; i < TAG_MAX_V; ++i) {
+    const int k = lane * 4 + 128 * i;
+    hv[i] = k < H ? __ldcs(reinterpret_cast<const float4*>(h + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float lg[HEAD_MAX_LABELS];
-  for (int l = 0; l < L; ++l) lg[l] = __fadd_rn(warp_dot(h, p.head_wt + size_t(l) * H, H), p.head_b[l]);
+  for (int l = 0; l < L; ++l) {
+    const float* w = p.head_wt + size_t(l) * H;
+    float acc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < TAG_MAX_V; ++i) {
+      const int k = lane * 4 + 128 * i;
+      if (k < H) {
+        const float4 y = __ldg(reinterpret_cast<const float4*>(w + k));
+        acc = __fmaf_rn(hv[i].x, y.x, acc);
+        acc = __fmaf_rn(hv[i].y, y.y, acc);
+        acc = __fmaf_rn(hv[i].z, y.z, acc);
+        acc = __fmaf_rn(hv[i].w, y.w, acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    lg[l] = __fadd_rn(acc, p.head_b[l]);
+  }
   if (threadIdx.x % 32 == 0) {
     float pr[HEAD_MAX_LABELS];
     int lab;

@@ -160,6 +160,25 @@ struct AttRow {
   bool live;            // the row is a real query
 };
 
+// the same row geometry from already-loaded sequence values (S = sequence length, att = the
+// attention length of this row's sequence): arithmetic only
+__device__ __forceinline__ AttRow att_row_of(int S, int att, int cnt, int r, int h) {
+  AttRow w;
+  w.h = h;
+  w.r = r;
+  w.S = S;
+  w.nk = cnt * S;
+  w.nkp = (w.nk + 31) & ~31;
+  w.nchunks = (w.nkp + ATT_P_CHUNK - 1) / ATT_P_CHUNK;
+  const int sub = cnt > 1 ? min(r / S, cnt - 1) : 0;
+  w.kbeg = sub * S;
+  w.att = att;
+  w.live = cnt > 1 ? r < w.nk : r < S;
+  return w;
+}
+// packed-tile row index of query row r (which sequence of the tile's cnt it belongs to)
+__device__ __forceinline__ int att_sub(int S, int cnt, int r) { return cnt > 1 ? min(r / S, cnt - 1) : 0; }
+
 template <int TPR>
 __device__ __forceinline__ AttRow att_row(const AttnParams& p, int seq, int q0, int cnt, int r, int h) {
   AttRow w;

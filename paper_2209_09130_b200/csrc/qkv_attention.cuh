@@ -67,6 +67,14 @@ struct QAParams {
   int late_trigger;        // measurement: keep the end-of-MMA trigger with tile_done set
 };
 
+// softmax warps' waits on the MMA results (s_full, o_full): parked try_wait by default;
+// SAMP_QA_SPIN builds a test_wait spin (measurement)
+#ifdef SAMP_QA_SPIN
+#define QA_SOFT_WAIT(bar, par) do { while (!mbar_test(bar, par)) {} } while (0)
+#else
+#define QA_SOFT_WAIT(bar, par) mbar_wait_park(bar, par)
+#endif
+
 template <int TPR>
 __global__ void __launch_bounds__(qa_threads<TPR>(), 1)
 qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w,
@@ -197,6 +205,7 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
             mma_ss<KIND_I8>(tmem + QA_TMEM_O, sdesc_k_sw128(pa + key), sdesc_mn_sw64(va + key * 64), idesc_o,
                             key != 0);
           mma_commit(o_full);
+          if (rec(m2)) rec(m2)[15] = globaltimer();
           ++m2;
           if (m2 < my) nk2 = m2 == m1 ? nk1 : tile_keys(item_tile(m2));
           did = true;
@@ -320,25 +329,43 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     };
     // j = -1 only runs the first item's epilogue (one inlined copy of each phase: the
     // kernel's code must stay small for the instruction cache)
+    // item geometry one item ahead (three levels of dependent global loads, ~1 us): the
+    // tile's sequence before the next item's epilogue, the sequence's rows and attention
+    // length before this item's ctx, the row geometry from registers at the loop top
+    int tn = item_tile(0), seqn = p.tile_seq[tn], cntn = p.tile_cnt[tn];
+    int k0n = p.seq_start[seqn], Sn = p.seq_start[seqn + 1] - k0n;
+    int attn = p.att_len[seqn + att_sub(Sn, cntn, r)];
 #pragma unroll 1
     for (int j = -1; j < my; ++j) {
       const int jc = j < 0 ? 0 : j;
-      const int t = item_tile(jc), head = item_head(jc);
-      const int seq = p.tile_seq[t];
-      const AttRow w = att_row<TPR>(p, seq, 0, p.tile_cnt[t], r, h);
-      const size_t ctx_row = size_t(p.seq_start[seq] + r);
+      const int t = tn, head = item_head(jc);
+      const AttRow w = att_row_of(Sn, attn, cntn, r, h);
+      const size_t ctx_row = size_t(k0n + r);
       unsigned long long* st = threadIdx.x == 32 * QA_SOFT_WARP0 && j >= 0 ? rec(j) : nullptr;
       if (j >= 0) {
-        mbar_wait_park(s_full, j & 1);
+#ifdef SAMP_QA_STAMP_PRESOFT   // measurement: st[0] := reached the s_full wait (overwrites epi_wait)
+        if (st) st[0] = globaltimer();
+#endif
+        QA_SOFT_WAIT(s_full, j & 1);
         tc_fence_after();
         if (st) st[3] = globaltimer();
         att_softmax_rr<TPR>(p, w, tmem + QA_TMEM_S + lane_base, smem + Lay::P_OFF, smem + Lay::X_OFF, p_full,
                             st ? st + 1 : nullptr);
       }
+      if (j >= 0 && j + 1 < my) {   // next item: its tile's sequence
+        tn = item_tile(j + 1);
+        seqn = p.tile_seq[tn];
+        cntn = p.tile_cnt[tn];
+      }
       // the next item's codes while MMA-2 of this one runs (its MMA-1 then only waits for ctx)
       if (j + 1 < my) epilogue(j + 1, threadIdx.x == 32 * QA_SOFT_WARP0 ? rec(j + 1) : nullptr);
       if (j < 0) continue;
-      mbar_wait_park(o_full, j & 1);
+      if (j + 1 < my) {   // next item: the sequence's rows and attention length
+        k0n = p.seq_start[seqn];
+        Sn = p.seq_start[seqn + 1] - k0n;
+        attn = p.att_len[seqn + att_sub(Sn, cntn, r)];
+      }
+      QA_SOFT_WAIT(o_full, j & 1);
       tc_fence_after();
       if (st) st[8] = globaltimer();
       att_ctx_out<false, TPR>(p, w, tmem + QA_TMEM_O + lane_base, ctx_row, head, 0.0f);

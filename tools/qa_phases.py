@@ -87,7 +87,7 @@ def main():
         print(f"item {j}: n={len(v)}  " + "  ".join(f"{l}={x:.2f}" for l, x in zip(labels, m)) +
               f"  | gemm_start={m[10]:.2f} ctx_done={m[11]:.2f} (max {v[:, 11].max():.2f})")
     names = ["epi_wait", "acc_ready", "epi_done", "soft_start", "pass1", "pass2", "sum", "p_done", "o_ready",
-             "ctx_done", "gemm_issue", "gemm_issued", "mma1_issued", "ctx_last", "epi_last"]
+             "ctx_done", "gemm_issue", "gemm_issued", "mma1_issued", "ctx_last", "epi_last", "mma2_issued"]
     print("absolute (us after the CTA's first stamp), mean over CTAs:")
     for j in range(4):
         vals = []
@@ -97,7 +97,7 @@ def main():
                 if r[9] == 0:
                     continue
                 b0 = st[b, 0][st[b, 0] > 0].min()
-                vals.append([(x - b0) / 1e3 if x else np.nan for x in r[:15]])
+                vals.append([(x - b0) / 1e3 if x else np.nan for x in r[:16]])
         if vals:
             m = np.nanmean(np.array(vals), 0)
             print(f"item {j}: " + "  ".join(f"{n}={v:.2f}" for n, v in zip(names, m)))

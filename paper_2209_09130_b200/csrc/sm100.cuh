@@ -51,7 +51,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #define SAMP_MBAR_HINT_NS 0
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#if SAMP_MBAR_HINT_NS > 0
+#if defined(SAMP_MBAR_SPIN)   // measurement: test_wait spin
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n"
+      :: "r"(smem_addr(bar)), "r"(parity) : "memory");
+#elif SAMP_MBAR_HINT_NS > 0
   asm volatile(
       "{\n .reg .pred P1;\n"
       "WAIT_%=:\n"

@@ -41,7 +41,7 @@ struct PersistLayout {
   static constexpr int B_OFF = STAGES * A_BYTES;
   static constexpr int BAR_OFF = B_OFF + STAGES * B_BYTES;             // full, empty, acc_full[2], acc_empty[2]
   static constexpr int EPI_STRIDE = (EPI_BYTES - TABLE_BYTES + 127) & ~127;   // per-buffer part
-  static constexpr int TBL_OFF = (BAR_OFF + 8 * (2 * STAGES + 4) + 8 + 127) & ~127;
+  static constexpr int TBL_OFF = (BAR_OFF + 8 * (2 * STAGES + 6) + 8 + 127) & ~127;   // + bias_full[2]
   static constexpr int EPI_OFF = TBL_OFF + ((TABLE_BYTES + 127) & ~127);
   static constexpr int TOTAL = EPI_OFF + 2 * EPI_STRIDE + 1024;
 };
@@ -71,7 +71,8 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* bias_full = acc_empty + 2;   // [2] tile bias landed in epilogue buffer b (bulk copy)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bias_full + 2);
   uint8_t* epi_smem = smem + Lay::EPI_OFF;
 
   const uint32_t warp = warp_id();
@@ -106,6 +107,7 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], NE);
+      mbar_init(&bias_full[b], 1);
     }
     fence_barrier_init();
   }
@@ -167,6 +169,13 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         stamp(j, 3);
+        // the tile's bias into epilogue buffer b: its readers (tile j-2's epilogue) are done
+        // once they released the accumulator buffer.  One bulk copy, completing bias_full[b]:
+        // no per-tile staging or barrier among the epilogue warps.
+        if constexpr (Epi::kStagedBias) {
+          mbar_expect_tx(&bias_full[b], BN * 4);
+          bulk_load(epi_smem + b * Lay::EPI_STRIDE + EPI_BIAS_OFF, ep.bias + tile_n0(j), BN * 4, &bias_full[b]);
+        }
         const uint32_t d = tmem + uint32_t(b * BN);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
@@ -192,33 +201,23 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
     const int tile_row = quarter * 32 + lane_id();
     const int c0 = part * (BN / PARTS);
     pdl_wait();
-    // both buffers: read-only tables + the first two tiles' bias
-    if constexpr (TBL > 0) {   // the shared table once, each buffer its tile's bias
+    // read-only tables once (the staged-bias epilogues get each tile's bias by the MMA
+    // warp's bulk copy; others stage their per-buffer operands here)
+    if constexpr (TBL > 0) {
       load_tanh_table(reinterpret_cast<TanhTable*>(smem + Lay::TBL_OFF), ep_tid, 32 * NE);
-      for (int b = 0; b < 2 && b < my_tiles; ++b)
-        stage_floats_async(reinterpret_cast<float*>(epi_smem + b * Lay::EPI_STRIDE), ep.bias + tile_n0(b), BN, ep_tid,
-                           32 * NE);
-      cp_async_commit();
-      cp_async_wait_all();
-    } else {
+    } else if constexpr (!Epi::kStagedBias) {
       for (int b = 0; b < 2 && b < my_tiles; ++b)
         Epi::template prefetch<BN>(ep, epi_smem + b * Lay::EPI_STRIDE, tile_m0(b), tile_n0(b), M, ep_tid, 32 * NE);
     }
     epi_bar_sync(32 * NE);
     for (int j = 0; j < my_tiles; ++j) {
       const int b = j & 1;
-      // stage tile j+1's bias into the other buffer (its last reader, tile j-1, is done)
-      if (Epi::kStagedBias && j >= 1 && j + 1 < my_tiles) {
-        float* dst = reinterpret_cast<float*>(epi_smem + ((j + 1) & 1) * Lay::EPI_STRIDE + EPI_BIAS_OFF);
-        const float* src = ep.bias + tile_n0(j + 1);
-        for (int i = ep_tid; i < BN / 4; i += 32 * NE) cp_async16(dst + 4 * i, src + 4 * i);
-        cp_async_commit();
-      }
       // the tile's coordinates (runtime div/mod) while the accumulator is still in flight
       const int m0 = tile_m0(j), n0 = tile_n0(j);
       if (ep_tid == 0) stamp(j, 0);
       mbar_wait(&acc_full[b], (j >> 1) & 1);
       tc_fence_after();
+      if constexpr (Epi::kStagedBias) mbar_wait(&bias_full[b], (j >> 1) & 1);
       if (ep_tid == 0) stamp(j, 1);
       EpiCtx c{tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * BN + c0), m0 + tile_row, tile_row, n0, c0,
                BN / PARTS, part, M, ep_tid, 32 * NE};
@@ -227,10 +226,6 @@ gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
-      if constexpr (Epi::kStagedBias) {
-        cp_async_wait_all();
-        epi_bar_sync(32 * NE);
-      }
       if (ep_tid == 0) stamp(j, 2);
     }
   }

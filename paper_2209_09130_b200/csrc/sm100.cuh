@@ -187,6 +187,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
          "r"(smem_addr(bar))
       : "memory");
 }
+// bulk (non-tensor) copy global -> this CTA's smem, completing `bytes` on an mbarrier
+// (16-byte aligned addresses, size a multiple of 16)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_addr(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
 // TMA tile store smem -> global (bulk group): the whole box in one instruction, clipped at the
 // tensor's bounds; the issuing thread waits for the smem reads before the buffer is reused
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {

@@ -128,7 +128,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   constexpr int TMEM_COLS = tmem_cols_for(BN);
   constexpr uint32_t IDESC = KIND == KIND_I8 ? idesc_i8(GEMM_BM, BN) : idesc_f16(GEMM_BM, BN);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
-  static_assert(NE == 4 || (NE == 8 && ((BN / 2) % 32 == 0 || BN == 96)), "epilogue split");
+  static_assert(NE == 4 || (NE == 8 && ((BN / 2) % 32 == 0 || BN == 96)) || (NE == 16 && BN == 192), "epilogue split");
   constexpr bool MCAST = MC && CLUSTER > 1;
   constexpr int A_ROWS = GEMM_BM / (MCAST ? CLUSTER : 1);   // rows of A this CTA loads
   constexpr uint16_t MASK = uint16_t((1u << CLUSTER) - 1);
@@ -249,7 +249,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   } else {
     const int ep_tid = threadIdx.x - GEMM_EPI_WARP0 * 32;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int half = NE == 8 ? int(warp - GEMM_EPI_WARP0) / 4 : 0;
+    const int half = NE >= 8 ? int(warp - GEMM_EPI_WARP0) / 4 : 0;   // NE = 16: quarter rows 0..3
     const int tile_row = quarter * 32 + lane_id();
     const int c0 = half * (BN / (NE / 4));
     if constexpr (KS2) {
@@ -731,7 +731,7 @@ struct EpiResLNT {
   // smem: [0,512) floats reduction scratch (per-half partials, 2 x CTA partials), then
   // bias / gamma / beta slices (BN floats each), then the int8 residual tile
   // [128][BN + 16] (16-byte row pad: conflict-free 16 B reads by consecutive rows)
-  static constexpr int RED_FLOATS = 4 * 128;
+  static constexpr int RED_FLOATS = 8 * 128;   // two reductions x up to 4 partials per row
   template <int BN> __host__ __device__ static constexpr int res_ld() { return BN + 16; }
   // cluster exchange (CLUSTER > 1): xpart [2 reductions][4][128] floats + xbar[2] mbarriers
   template <int BN> __host__ __device__ static constexpr int xp_off() { return (RED_FLOATS + 3 * BN) * 4 + 128 * res_ld<BN>(); }
@@ -787,6 +787,12 @@ struct EpiResLNT {
       hv[c.half * 128 + c.tile_row] = mine;
       epi_bar_sync(c.ne_threads);
       s = __fadd_rn(hv[c.tile_row], hv[128 + c.tile_row]);
+    } else if constexpr (NE == 16) {    // two leaves x two accumulator halves (run_strided)
+      float* hv = halves + red * 512;
+      hv[c.half * 128 + c.tile_row] = mine;
+      epi_bar_sync(c.ne_threads);
+      s = __fadd_rn(__fadd_rn(hv[c.tile_row], hv[128 + c.tile_row]),
+                    __fadd_rn(hv[256 + c.tile_row], hv[384 + c.tile_row]));
     }
     if constexpr (CLUSTER > 1) {
       float* xp = reinterpret_cast<float*>(smem + xp_off<BN>()) + red * XP_MAX * 128;
@@ -1154,7 +1160,10 @@ struct EpiResLNT {
   // values in registers; normalisation and outputs run on 4-column groups.
   template <int BN, int CLUSTER, int NE>
   __device__ static void run_strided(const Params& p, const EpiCtx& c, uint8_t* smem) {
-    static_assert(BN == 96 && NE == 8, "one 96-column leaf split over two threads");
+    // NE = 16, BN = 192 (small hidden, 4-CTA clusters): two 96-column leaves per CTA, each
+    // split the same way over two of the row's four threads (quarter q: leaf q >> 1, half q & 1)
+    static_assert((BN == 96 && NE == 8) || (BN == 192 && NE == 16), "96-column leaves, two threads each");
+    constexpr int LEAF = 96;
     float* halves = reinterpret_cast<float*>(smem);
     const float* sbias = halves + RED_FLOATS;
     const float* sgam = sbias + BN;
@@ -1162,31 +1171,35 @@ struct EpiResLNT {
     const uint8_t* rtile = smem + (RED_FLOATS + 3 * BN) * 4 + c.tile_row * res_ld<BN>();
     const bool valid = c.row < c.M;
     const size_t rbase = size_t(valid ? c.row : 0) * p.hidden;
-    const int jo = 4 * c.half;
-    const uint32_t tbase = c.taddr - uint32_t(c.c0);
+    const int hh = c.half & 1;                 // accumulator half within the leaf
+    const int lbase = LEAF * (c.half >> 1);    // the leaf's first tile column
+    const int jo = 4 * hh;
+    const uint32_t tbase = c.taddr - uint32_t(c.c0) + uint32_t(lbase);
     float x[48];
-    // the register index must be compile-time: one body per half
+    if (c.kpart) mbar_wait(c.kpart_bar, 0);    // KS2: the other K half's accumulators landed
+    // the register index must be compile-time: one body per half; 32 TMEM columns at a time
     auto fill = [&](auto jo_c) {
       constexpr int JO = decltype(jo_c)::value;
-      uint32_t r[96];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) tmem_ld32(tbase + 32 * k, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * k));
+      for (int k = 0; k < 3; ++k) {
+      uint32_t r[32];
+      tmem_ld32(tbase + 32 * k, r);
       tmem_wait_ld();
       if (c.kpart) {   // KS2: add the other K half's accumulators (int32 exact; f32 for kind::f16)
-        mbar_wait(c.kpart_bar, 0);
-        const uint32_t* kp = c.kpart + c.tile_row * BN;
+        const uint32_t* kp = c.kpart + c.tile_row * BN + lbase + 32 * k;
 #pragma unroll
-        for (int g = 0; g < 12; ++g)
+        for (int gg = 0; gg < 4; ++gg)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int j = 8 * g + JO + u;
+            const int j = 8 * gg + JO + u;
             r[j] = p.acc_is_f32 ? __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __uint_as_float(kp[j])))
                                 : uint32_t(int(r[j]) + int(kp[j]));
           }
       }
 #pragma unroll
-      for (int g = 0; g < 12; ++g) {
-        const int col = 8 * g + JO;
+      for (int gg = 0; gg < 4; ++gg) {
+        const int g = 4 * k + gg;
+        const int col = lbase + 8 * g + JO;
         float res[4];
         if (p.res_i8) {
           const uint32_t w = *reinterpret_cast<const uint32_t*>(rtile + col);
@@ -1204,14 +1217,15 @@ struct EpiResLNT {
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t a = r[col + u];
+          const uint32_t a = r[8 * gg + JO + u];
           const float acc = p.acc_is_f32 ? __uint_as_float(a) : __fmul_rn(__int2float_rn(int(a)), p.mult);
           x[4 * g + u] = __fadd_rn(__fadd_rn(acc, sbias[col + u]), res[u]);
         }
       }
+      }
     };
     if (p.tma_res) mbar_wait(res_bar<BN>(smem), 0);
-    if (c.half == 0) fill(std::integral_constant<int, 0>{});
+    if (hh == 0) fill(std::integral_constant<int, 0>{});
     else fill(std::integral_constant<int, 4>{});
     auto half_leaf = [&](auto f) {
       float a[4];
@@ -1247,7 +1261,7 @@ struct EpiResLNT {
       const float2 nm = f2(-mean, -mean), iv = f2(inv, inv);
 #pragma unroll
       for (int g = 0; g < 12; ++g) {
-        const int col = 8 * g + jo;
+        const int col = lbase + 8 * g + jo;
         const float4 g4 = *reinterpret_cast<const float4*>(sgam + col);
         const float4 b4 = *reinterpret_cast<const float4*>(sbet + col);
         float2 q[2];
@@ -1266,7 +1280,7 @@ struct EpiResLNT {
     } else if (valid) {
 #pragma unroll
       for (int g = 0; g < 12; ++g) {
-        const int col = 8 * g + jo;
+        const int col = lbase + 8 * g + jo;
         const size_t o = rbase + c.n0 + col;
         float y[4];
 #pragma unroll
@@ -1346,7 +1360,7 @@ struct EpiResLNT {
 
   template <int BN, int CLUSTER, int NE>
   __device__ static void run(const Params& p, const EpiCtx& c, uint8_t* smem) {
-    if constexpr (NE == 8 && BN == 96) {
+    if constexpr ((NE == 8 && BN == 96) || (NE == 16 && BN == 192)) {
       run_strided<BN, CLUSTER, NE>(p, c, smem);
       return;
     }

@@ -35,6 +35,8 @@ cudaError_t gemm_ln_i8(const Tiles& t, const CUtensorMap& a, const CUtensorMap& 
     switch (t.bn_ln * 10 + t.cluster_ln) {
       case 1924:
         if (mc) return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8, true>(a_mc[0], b, M, N, kb, q, st);
+        // 16 epilogue warps: four threads per row, two per 96-column numpy leaf (run_strided)
+        if (env_flag("SAMP_LN_NE16")) return launch_gemm<KIND_I8, 192, 4, 4, 16, EpiResLNI8>(a, b, M, N, kb, q, st);
         return launch_gemm<KIND_I8, 192, 4, 4, 8, EpiResLNI8>(a, b, M, N, kb, q, st);
       case 2564: return launch_gemm<KIND_I8, 256, 3, 4, 8, EpiResLNI8>(a, b, M, N, kb, q, st);
     }

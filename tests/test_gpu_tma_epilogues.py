@@ -19,7 +19,7 @@ from paper_2209_09130_b200.tokenization import EncodedInput
 
 pytestmark = pytest.mark.gpu
 
-SWITCHES = ("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES", "SAMP_LN96_STRIDED")
+SWITCHES = ("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES", "SAMP_LN96_STRIDED", "SAMP_LN_NE16", "SAMP_LN_NE8")
 
 
 @pytest.fixture(scope="module")
@@ -64,7 +64,8 @@ def test_tma_epilogue_variants_bit_identical(arch2, monkeypatch, mode, k, fp16, 
     encs = _encs(batch, 128 if batch != 5 else 100, batch)   # batch 5 x 100: a ragged last row tile
     plan = PrecisionPlan.prefix(mode, 2, k)
     base = _run(arch2, encs, plan, monkeypatch, (), fp16)
-    for env in (("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES"), ("SAMP_LN96_STRIDED",)):
+    for env in (("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES"), ("SAMP_LN96_STRIDED",), ("SAMP_LN_NE16",),
+                ("SAMP_LN_NE8",)):
         other = _run(arch2, encs, plan, monkeypatch, env, fp16)
         np.testing.assert_array_equal(base, other, err_msg=f"{mode} batch {batch} {env}")
 

@@ -3,7 +3,8 @@
 The LN GEMMs write their tiles through shared memory and TMA stores (int8 codes; small-batch
 f32/f16 outputs in 128B/64B-swizzled boxes) and, at small batches, take the f32 residual
 tile by TMA into the drained operand ring.  The arithmetic is unchanged, so every variant
-(switches read per launch; a fresh engine per variant, no captured graph carried over)
+(switches read per launch; a fresh engine per variant, no captured graph carried over; and
+the 16-epilogue-warp LN variant, SAMP_LN_NE16)
 must give the same hidden states bit for bit, for INT8 and FP16 plans, batch 1 (8-CTA
 clusters) and batch 32 (4-CTA clusters), and a ragged final row tile.
 """
@@ -19,7 +20,7 @@ from paper_2209_09130_b200.tokenization import EncodedInput
 
 pytestmark = pytest.mark.gpu
 
-SWITCHES = ("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES", "SAMP_LN96_STRIDED", "SAMP_LN_NE16", "SAMP_LN_NE8")
+SWITCHES = ("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES", "SAMP_LN96_STRIDED", "SAMP_LN_NE16")
 
 
 @pytest.fixture(scope="module")
@@ -64,8 +65,7 @@ def test_tma_epilogue_variants_bit_identical(arch2, monkeypatch, mode, k, fp16, 
     encs = _encs(batch, 128 if batch != 5 else 100, batch)   # batch 5 x 100: a ragged last row tile
     plan = PrecisionPlan.prefix(mode, 2, k)
     base = _run(arch2, encs, plan, monkeypatch, (), fp16)
-    for env in (("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES"), ("SAMP_LN96_STRIDED",), ("SAMP_LN_NE16",),
-                ("SAMP_LN_NE8",)):
+    for env in (("SAMP_NO_LN_TMA_STORE", "SAMP_NO_LN_TMA_RES"), ("SAMP_LN96_STRIDED",), ("SAMP_LN_NE16",)):
         other = _run(arch2, encs, plan, monkeypatch, env, fp16)
         np.testing.assert_array_equal(base, other, err_msg=f"{mode} batch {batch} {env}")
 

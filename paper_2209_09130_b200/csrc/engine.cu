@@ -1583,8 +1583,10 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       if (e->pinned_cap < 2 * T) {
         if (e->pinned_ids) cudaFreeHost(e->pinned_ids);
         e->pinned_ids = nullptr;
-        e->pinned_cap = std::max(2 * T, 8192);
-        SAMP_CUDA(cudaMallocHost(&e->pinned_ids, size_t(e->pinned_cap) * sizeof(int)));
+        e->pinned_cap = 0;   // set only once the allocation succeeded
+        const int cap = std::max(2 * T, 8192);
+        SAMP_CUDA(cudaMallocHost(&e->pinned_ids, size_t(cap) * sizeof(int)));
+        e->pinned_cap = cap;
       }
       SAMP_CUDA(cudaStreamSynchronize(st));  // staging buffer reuse
       std::memcpy(e->pinned_ids, ids, size_t(T) * 4);
@@ -1645,8 +1647,11 @@ extern "C" int samp_forward(samp_engine* e, const uint8_t* prec, int32_t nseq, c
       if (staged) {   // the three head outputs are contiguous on the device: one D2H
         if (e->pinned_out_cap < head_bytes) {
           if (e->pinned_out) cudaFreeHost(e->pinned_out);
-          e->pinned_out_cap = std::max<size_t>(head_bytes, 1 << 16);
-          SAMP_CUDA(cudaMallocHost(&e->pinned_out, e->pinned_out_cap));
+          e->pinned_out = nullptr;   // a failed allocation below must not leave a freed pointer
+          e->pinned_out_cap = 0;
+          const size_t cap = std::max<size_t>(head_bytes, 1 << 16);
+          SAMP_CUDA(cudaMallocHost(&e->pinned_out, cap));
+          e->pinned_out_cap = cap;
         }
         SAMP_CUDA(cudaMemcpyAsync(e->pinned_out, a.headbuf, head_bytes, cudaMemcpyDeviceToHost, st));
       } else if (head != SAMP_HEAD_NONE) {

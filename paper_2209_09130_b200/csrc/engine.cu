@@ -963,6 +963,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     auto ok = e->gelu_fast_ok.find(bits_of(gp.s_out));
     const bool fast = finite && ok != e->gelu_fast_ok.end() && ok->second;
     gp.inv_s = gelu_inv_s(gp.s_out);
+    gp.fixup_all = env_flag("SAMP_GELU_FIXUP_ALL");   // test: every 8-group through gelu_fixup
     if (env_flag("SAMP_GELU_FLAGS")) {   // measurement: count flagged 8-groups per forward
       if (!g_gelu_flags) cudaMallocManaged(&g_gelu_flags, sizeof(unsigned long long));
       gp.flag_count = g_gelu_flags;

@@ -505,6 +505,7 @@ struct GeluQuantParams {
   float inv_s = 0.0f;   // ~1/s_out (GELU_FAST)
   X2 k = x2_consts();   // opaque FFMA2 constants (packed path)
   unsigned long long* flag_count = nullptr;   // measurement: flagged 8-groups (SAMP_GELU_FLAGS)
+  int fixup_all = 0;    // test switch (SAMP_GELU_FIXUP_ALL): every 8-group through gelu_fixup
 };
 template <int MODE>
 struct EpiGeluQuantT {
@@ -542,6 +543,7 @@ struct EpiGeluQuantT {
 #endif
     constexpr int COLS = BN / (NE / 4);
     constexpr int CH = COLS % SAMP_GELU_CHUNK == 0 ? SAMP_GELU_CHUNK : COLS % 16 == 0 ? 16 : 8;
+    uint32_t fmask = 0;   // GELU_FAST: bit col/8 = that 8-group was flagged (exact codes after the loop)
 #pragma unroll 1
     for (int col = 0; col < c.ncols; col += CH) {
       const int gcol = c.n0 + c.c0 + col;
@@ -579,12 +581,20 @@ struct EpiGeluQuantT {
 #ifdef SAMP_GELU_FLAG_COUNT   // measurement build only (costs ~1 us per FFN1 launch)
             if (near && p.flag_count) atomicAdd(p.flag_count, 1ull);
 #endif
+#ifdef SAMP_GELU_INLINE_FALLBACK   // measurement: the exact path inside the loop (round-2 form)
             if (near) {
               exact8(v, tt, rq, k, w[g / 4], w[g / 4 + 1]);
             } else {
               w[g / 4] = trunc_pack4_s8(t[0].x, t[0].y, t[1].x, t[1].y);
               w[g / 4 + 1] = trunc_pack4_s8(t[2].x, t[2].y, t[3].x, t[3].y);
             }
+#else
+            // flagged groups get their exact codes after the loop (gelu_fixup), so the exact
+            // path's code and registers stay out of the hot loop
+            if (near || p.fixup_all) fmask |= 1u << ((col + g) >> 3);
+            w[g / 4] = trunc_pack4_s8(t[0].x, t[0].y, t[1].x, t[1].y);
+            w[g / 4 + 1] = trunc_pack4_s8(t[2].x, t[2].y, t[3].x, t[3].y);
+#endif
           } else {
             exact8(v, tt, rq, k, w[g / 4], w[g / 4 + 1]);
           }
@@ -610,6 +620,42 @@ struct EpiGeluQuantT {
 #pragma unroll
           for (int q = 0; q < CH / 16; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
         }
+      }
+    }
+    if constexpr (MODE == GELU_FAST) {
+      const uint32_t any = __reduce_or_sync(0xffffffffu, fmask);   // warp-uniform: tcgen05.ld is .sync.aligned
+      if (any)
+        gelu_fixup(p.out + size_t(c.row) * p.ldo + c.n0 + c.c0, c.row < c.M,
+                   SAMP_BIAS_GLOBAL ? p.bias + c.n0 + c.c0 : sbias + c.c0, p.mult, p.k, c.taddr, tt, rq, fmask, any);
+    }
+  }
+  // Exact codes of the flagged 8-groups (~5e-4 of the groups on the bench batch): the warp
+  // walks the union of its threads' flagged groups, re-reads those 8 accumulator columns
+  // (still in TMEM: the buffer is released after run()), and each flagging thread recomputes
+  // its group on the bit-exact numpy/SVML path and overwrites the 8 fast codes it stored.
+  // (scalars only: a by-reference Params/EpiCtx would be copied to local memory per tile)
+  __device__ static __noinline__ void gelu_fixup(int8_t* out, bool live, const float* bias, float mult, const X2 k,
+                                                 uint32_t taddr, const TanhTable* tt, const Recip rq, uint32_t mine,
+                                                 uint32_t any) {
+    while (any) {
+      const int gi = __ffs(int(any)) - 1;
+      any &= any - 1;
+      const int col = gi * 8;
+      uint32_t r[8];
+      tmem_ld8(taddr + col, r);
+      tmem_wait_ld();
+      if ((mine >> gi) & 1u) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const float2 d = add2(mul2(f2(__int2float_rn(int(r[u])), __int2float_rn(int(r[u + 1]))), f2(mult, mult), k),
+                                f2(bias[col + u], bias[col + u + 1]), k);
+          v[u] = d.x;
+          v[u + 1] = d.y;
+        }
+        uint32_t w0, w1;
+        exact8(v, tt, rq, k, w0, w1);
+        if (live) *reinterpret_cast<uint2*>(out + col) = make_uint2(w0, w1);
       }
     }
   }

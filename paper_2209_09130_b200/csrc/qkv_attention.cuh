@@ -278,11 +278,15 @@ qkv_attention_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     constexpr int CW = 64 / TPR;
     auto epilogue = [&](int jj, unsigned long long* st) {
       const int b = jj & 1;
-      // the item's rows (dependent loads) before the accumulator wait
-      const int t = item_tile(jj), head = item_head(jj);
-      const int seq = p.tile_seq[t];
-      const int row0 = p.seq_start[seq];
-      const int rows = (p.seq_start[seq + 1] - row0) * p.tile_cnt[t];
+      const int head = item_head(jj);
+      // the item's rows (two dependent global loads) only for the stage capture: on the
+      // normal path nothing between the softmax and the accumulator wait touches memory
+      int row0 = 0, rows = 0;
+      if (q.qkv_out) {
+        const int t = item_tile(jj), seq = p.tile_seq[t];
+        row0 = p.seq_start[seq];
+        rows = (p.seq_start[seq + 1] - row0) * p.tile_cnt[t];
+      }
       if (st) st[0] = globaltimer();
       QA_ACC_WAIT(acc_full, jj & 1);
       tc_fence_after();

@@ -88,3 +88,24 @@ def test_ffn2_k_split_cluster(arch2, monkeypatch, mode, k, fp16, batch):
     else:
         rel = float(np.linalg.norm(got - base) / np.linalg.norm(base))
         assert rel < 1e-3, rel
+
+
+@pytest.mark.parametrize("batch", [1, 32, 5])
+def test_gelu_fixup_path_bit_exact(arch2, monkeypatch, batch):
+    """FFN1's fast GELU epilogue recomputes flagged 8-groups after its column loop
+    (EpiGeluQuantT::gelu_fixup: TMEM re-read, exact numpy/SVML codes overwrite the fast ones).
+    Flags are rare (~5e-4 of the groups), so SAMP_GELU_FIXUP_ALL sends EVERY group through
+    the fixup: the codes must not change, and they equal the oracle's."""
+    encs = _encs(batch, 128 if batch != 5 else 100, 40 + batch)
+    plan = PrecisionPlan.prefix("FULLY_QUANT", 2, 2)
+    base = _run(arch2, encs, plan, monkeypatch, ())
+    monkeypatch.setenv("SAMP_GELU_FIXUP_ALL", "1")
+    from paper_2209_09130_b200.engine import Engine
+    got = Engine(arch2).run_batch(encs, plan).hidden_states.copy()
+    monkeypatch.delenv("SAMP_GELU_FIXUP_ALL")
+    np.testing.assert_array_equal(got, base)
+    model = orc.Model.from_manifest(arch2.manifest, arch2.tensors,
+                                    {s: e.amax for s, e in arch2.calibration.entries.items()})
+    e = encs[0]
+    want = orc.run(model, e.token_ids, e.segment_ids, e.attention_length, plan.layer_precisions)
+    np.testing.assert_array_equal(got[:len(e.token_ids)], want)

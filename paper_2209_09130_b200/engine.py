@@ -23,7 +23,7 @@ from . import _lib
 from .archive import ModelArchive, layer_keys
 from .errors import CalibrationError, ConfigurationError, InputError
 from .plan import (EMBED_OUT_SITE, LAYER_CODE, LAYER_FP, PrecisionPlan, activation_sites)
-from .quantization import CalibrationTable, CodeUsageReport, QuantScale, quantize
+from .quantization import CalibrationTable, CodeUsageReport, QuantScale, quantize, scale_edit_count
 from .tokenization import EncodedInput, encode as encode_text
 from . import trace as _trace
 
@@ -113,6 +113,7 @@ class Engine:
         if self.exact_fp32:
             _lib.check(lib.samp_set_exact_fp32(self._h, 1))
         self._pushed_calibration = None
+        self._pushed_key = None
         self._push_calibration()
 
     def __del__(self):
@@ -136,17 +137,36 @@ class Engine:
         # a plain list in the dict's order (a reordered but equal table only costs a re-push)
         return [(s, e.amax) for s, e in table.entries.items()]
 
+    def _calibration_key(self):
+        """Cheap fingerprint of the table as it stands: the table and dict objects, the sites,
+        the QuantScale objects (C-level tuples, compared by identity first) and the
+        process-wide count of QuantScale attribute writes.  Any edit the reference would see
+        (an amax written, an entry added, replaced, deleted or re-keyed, the dict or the table
+        swapped) changes it; an unchanged key means the full snapshot is unchanged too."""
+        table = self.archive.calibration
+        if table is None:
+            return None
+        d = table.entries
+        return (id(table), id(d), tuple(d), tuple(d.values()), scale_edit_count())
+
     def _push_calibration(self) -> None:
-        """Send the table's amax values to the device when they differ from what it holds."""
+        """Send the table's amax values to the device when they differ from what it holds.
+        Per forward only the cheap key is compared; the full snapshot only when it moved."""
         with self._lock:
+            key = self._calibration_key()
+            if key is not None and key == self._pushed_key:
+                return
             state = self._calibration_state()
             if state == self._pushed_calibration:
+                self._pushed_key = key
                 return
             _lib.check(self._lib.samp_clear_calibration(self._h))
             self._pushed_calibration = None
+            self._pushed_key = None
             for site, amax in state or ():
                 _lib.check(self._lib.samp_set_site_amax(self._h, site.encode(), float(amax)))
             self._pushed_calibration = state
+            self._pushed_key = key
 
     def check_plan(self, plan: PrecisionPlan) -> CalibrationTable | None:
         """reference encoder.py:456-470 (same messages)."""

@@ -207,3 +207,39 @@ def test_encoder_module_mirrors_reference_names():
     sites = enc.activation_sites(2)
     assert sites[0] == "embed.out" and len(sites) == 1 + 8 * 2
     assert enc.ATTENTION_MASK_VALUE == np.float32(-10000.0)
+
+
+def test_calibration_key_tracks_every_table_edit():
+    """Engine._calibration_key (the per-forward check before the device amax push) must move on
+    every edit the reference's fresh read would see, and stay put otherwise."""
+    from paper_2209_09130_b200.engine import Engine
+    from paper_2209_09130_b200.quantization import CalibrationTable, QuantScale
+
+    class _E:
+        pass
+
+    table = CalibrationTable(model_fingerprint="x")
+    for i, s in enumerate(("L0.attn.q", "L0.attn.k", "L0.ffn.mid")):
+        table.set_amax(s, 1.0 + i)
+    e = _E()
+    e.archive = _E()
+    e.archive.calibration = table
+    key = lambda: Engine._calibration_key(e)   # noqa: E731
+    k = key()
+    assert key() == k
+    edits = [
+        lambda: setattr(table.entries["L0.ffn.mid"], "amax", 7.0),                       # in-place amax
+        lambda: table.entries.__setitem__("L0.attn.q", QuantScale("L0.attn.q", 1.0)),    # replaced object
+        lambda: table.entries.update({"L0.attn.q": table.entries["L0.attn.k"],
+                                      "L0.attn.k": table.entries["L0.attn.q"]}),          # swapped objects
+        lambda: table.entries.pop("L0.attn.k"),                                           # deleted
+        lambda: setattr(table, "entries", dict(table.entries)),                           # dict replaced
+    ]
+    for edit in edits:
+        edit()
+        k2 = key()
+        assert k2 != k
+        k = k2
+        assert key() == k
+    e.archive.calibration = None
+    assert key() is None

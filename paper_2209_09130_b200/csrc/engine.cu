@@ -68,6 +68,7 @@ struct LayerDev {
   float *b1 = nullptr, *b2 = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
   double s_w[6] = {0, 0, 0, 0, 0, 0};  // qw kw vw ow w1 w2
   double b1_absmax = 0;                 // max|b1|: bounds the FFN1 GELU argument
+  bool ln1_bounded = false, ln2_bounded = false;   // |LN output| < 1e18 proved (EpiResLN noclamp)
   CUtensorMap m_qkv_i8, m_wo_i8, m_w2_i8, m_qkv_f16, m_wo_f16, m_w2_f16;
   CUtensorMap m_wo_i8_64, m_w2_i8_64;    // 64-row boxes: split-K GEMMs for small batches
   CUtensorMap m_wo_i8_s, m_w2_i8_s, m_wo_f16_s, m_w2_f16_s;   // bn_ln_small-row boxes
@@ -842,6 +843,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
     lp.res_scale = f32(s_in);
     lp.gamma = w.ln1_g;
     lp.beta = w.ln1_b;
+    lp.noclamp = w.ln1_bounded;
     lp.mult = mult_of(sc(e, lsite(i, "attn", "out_in")), w.s_w[3]);
     lp.eps = eps;
     lp.hidden = H;
@@ -940,6 +942,7 @@ static void run_layer(samp_engine* e, int i, const uint8_t* prec, int& cur) {
   EpiResLN::Params lp{};
   lp.gamma = w.ln2_g;
   lp.beta = w.ln2_b;
+  lp.noclamp = w.ln2_bounded;
   lp.eps = eps;
   lp.hidden = H;
   lp.bias = w.b2;
@@ -1248,6 +1251,20 @@ extern "C" int samp_load_layer(samp_engine* e, int layer, const float* const* t)
     w.b2 = up(t[13], H);
     w.ln2_g = up(t[14], H);
     w.ln2_b = up(t[15], H);
+    // |((x - mean) * inv) * g + b| <= sqrt(H) max|g| + max|b| (each |x - mean| <= sqrt(H var),
+    // inv = 1/sqrt(var + eps) with eps > 0), doubled for rounding: far below the 2^64 where
+    // the LN epilogue's fast quotient needs its clamp
+    auto ln_bounded = [&](const float* g, const float* b) {
+      double mg = 0, mb = 0;
+      for (int j = 0; j < H; ++j) {
+        if (!std::isfinite(g[j]) || !std::isfinite(b[j])) return false;
+        mg = std::max(mg, double(std::fabs(g[j])));
+        mb = std::max(mb, double(std::fabs(b[j])));
+      }
+      return e->d.layernorm_eps > 0 && 2.0 * std::sqrt(double(H)) * mg + mb < 1e18;
+    };
+    w.ln1_bounded = ln_bounded(t[8], t[9]);
+    w.ln2_bounded = ln_bounded(t[14], t[15]);
     const Tiles& tl = e->tiles;
     w.m_qkv_i8 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, tl.bn_qkv);
     w.m_qkv_i8_128 = tmap_i8(w.qkv_i8, 3 * H, H, H, 128, 128);

@@ -750,6 +750,8 @@ struct ResLNParams {
   float* tap_f32 = nullptr;       // capture_taps: [M][H] LayerNorm output before quantize
   X2 k = x2_consts();             // opaque FFMA2 constants (paired INT8 path, numerics.cuh)
   int tma_store = 0;              // I8_ONLY register path: the code tile leaves by one TMA store
+  int noclamp = 0;                // host proved |LN output| < 1e18 (2 sqrt(H) max|g| + max|b|, eps > 0):
+                                  // the +-2^64 clamp before the fast quotient is a no-op
   CUtensorMap out_map;            // ... over out_i8 [rows][hidden], box BN x 128, no swizzle
   // small-batch f32/f16 outputs (FP layers) by TMA: bit 0 out_f32 through map_f32 (box 32 x 128
   // f32, 128B swizzle), bit 1 out_f16 through map_f16 (box 32 x 128 f16, 64B swizzle)
@@ -1070,84 +1072,96 @@ struct EpiResLNT {
     float amx = 0.0f;
     uint32_t tw[I8_ONLY ? NC / 4 : 1];   // TMA-store path: this thread's codes
     if (valid || (I8_ONLY && p.tma_store)) {
+      // the +-2^64 clamp compiled out when the host proved it a no-op (p.noclamp): a runtime
+      // test inside the loop was only predicated, not removed
+      auto emit_rows = [&](auto clamp_tag) {
+        constexpr bool CLAMP = decltype(clamp_tag)::value;
 #pragma unroll
-      for (int k = 0; k < NC / 32; ++k) {
-        if constexpr (I8_ONLY) {
-          // y = ((x - mean)*inv)*g + b and quantize on FFMA2 pairs, γ/β as float4
-          const X2 kx = p.k;
-          const float2 nm = f2(-mean, -mean), iv = f2(inv, inv);
-          uint32_t w[8];
+        for (int k = 0; k < NC / 32; ++k) {
+          if constexpr (I8_ONLY) {
+            // y = ((x - mean)*inv)*g + b and quantize on FFMA2 pairs, γ/β as float4
+            const X2 kx = p.k;
+            const float2 nm = f2(-mean, -mean), iv = f2(inv, inv);
+            uint32_t w[8];
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const int col = c.c0 + 32 * k + 4 * g;
-            const float4 g4 = *reinterpret_cast<const float4*>(sgam + col);
-            const float4 b4 = *reinterpret_cast<const float4*>(sbet + col);
-            float2 q[2];
+            for (int g = 0; g < 8; ++g) {
+              const int col = c.c0 + 32 * k + 4 * g;
+              const float4 g4 = *reinterpret_cast<const float4*>(sgam + col);
+              const float4 b4 = *reinterpret_cast<const float4*>(sbet + col);
+              float2 q[2];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int j = 32 * k + 4 * g + 2 * u;
-              float2 y = mul2(mul2(add2(f2(x[j], x[j + 1]), nm, kx), iv, kx),
-                              u ? f2(g4.z, g4.w) : f2(g4.x, g4.y), kx);
-              y = add2(y, u ? f2(b4.z, b4.w) : f2(b4.x, b4.y), kx);
-              y = f2(fminf(fmaxf(y.x, -1.8446744e19f), 1.8446744e19f), fminf(fmaxf(y.y, -1.8446744e19f), 1.8446744e19f));
-              q[u] = quant_pre2(y, rq, kx);
-            }
-            w[g] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
-          }
-          if (p.tma_store) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) tw[8 * k + u] = w[u];
-            continue;
-          }
-          uint4* dst = reinterpret_cast<uint4*>(p.out_i8 + rbase + c.n0 + c.c0 + 32 * k);
-#ifdef SAMP_EXP_LN_NOSTORE   // measurement variant only: results garbage
-          if ((w[0] ^ w[1] ^ w[2] ^ w[3] ^ w[4] ^ w[5] ^ w[6] ^ w[7]) == 0x12345678u)
-#endif
-          {
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          }
-        } else {
-          float y[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = c.c0 + 32 * k + j;
-            y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[32 * k + j], mean), inv), sgam[col]), sbet[col]);
-          }
-          if (p.tma_f) {
-            // stage 32 columns: f32 box k (128 B rows, 128B swizzle: chunk ^ (row & 7)) and
-            // f16 box k (64 B rows, 64B swizzle: chunk ^ ((row >> 1) & 3)); the XOR acts on
-            // addresses, so the register indices stay compile-time
-            if (p.f16_round) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
-            }
-            if (p.tma_f & 1) {
-              uint8_t* rowp = c.stage + k * (128 * 128) + c.tile_row * 128;
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                *reinterpret_cast<float4*>(rowp + ((q ^ (c.tile_row & 7)) << 4)) =
-                    make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
-            }
-            if (p.tma_f & 2) {
-              uint8_t* rowp = c.stage + 3 * (128 * 128) + k * (128 * 64) + c.tile_row * 64;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t hw[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  __half2 h2 = __floats2half2_rn(y[8 * q + 2 * u], y[8 * q + 2 * u + 1]);
-                  hw[u] = *reinterpret_cast<uint32_t*>(&h2);
-                }
-                *reinterpret_cast<uint4*>(rowp + ((q ^ ((c.tile_row >> 1) & 3)) << 4)) =
-                    make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              for (int u = 0; u < 2; ++u) {
+                const int j = 32 * k + 4 * g + 2 * u;
+                float2 y = mul2(mul2(add2(f2(x[j], x[j + 1]), nm, kx), iv, kx),
+                                u ? f2(g4.z, g4.w) : f2(g4.x, g4.y), kx);
+                y = add2(y, u ? f2(b4.z, b4.w) : f2(b4.x, b4.y), kx);
+                if constexpr (CLAMP)
+                  y = f2(fminf(fmaxf(y.x, -1.8446744e19f), 1.8446744e19f), fminf(fmaxf(y.y, -1.8446744e19f), 1.8446744e19f));
+                q[u] = quant_pre2(y, rq, kx);
               }
+              w[g] = trunc_pack4_s8(q[0].x, q[0].y, q[1].x, q[1].y);
+            }
+            if (p.tma_store) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) tw[8 * k + u] = w[u];
+              continue;
+            }
+            uint4* dst = reinterpret_cast<uint4*>(p.out_i8 + rbase + c.n0 + c.c0 + 32 * k);
+#ifdef SAMP_EXP_LN_NOSTORE   // measurement variant only: results garbage
+            if ((w[0] ^ w[1] ^ w[2] ^ w[3] ^ w[4] ^ w[5] ^ w[6] ^ w[7]) == 0x12345678u)
+#endif
+            {
+              dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
             }
           } else {
-            emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+            float y[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = c.c0 + 32 * k + j;
+              y[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x[32 * k + j], mean), inv), sgam[col]), sbet[col]);
+            }
+            if (p.tma_f) {
+              // stage 32 columns: f32 box k (128 B rows, 128B swizzle: chunk ^ (row & 7)) and
+              // f16 box k (64 B rows, 64B swizzle: chunk ^ ((row >> 1) & 3)); the XOR acts on
+              // addresses, so the register indices stay compile-time
+              if (p.f16_round) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[j] = __half2float(__float2half_rn(y[j]));
+              }
+              if (p.tma_f & 1) {
+                uint8_t* rowp = c.stage + k * (128 * 128) + c.tile_row * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  *reinterpret_cast<float4*>(rowp + ((q ^ (c.tile_row & 7)) << 4)) =
+                      make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+              }
+              if (p.tma_f & 2) {
+                uint8_t* rowp = c.stage + 3 * (128 * 128) + k * (128 * 64) + c.tile_row * 64;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  uint32_t hw[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    __half2 h2 = __floats2half2_rn(y[8 * q + 2 * u], y[8 * q + 2 * u + 1]);
+                    hw[u] = *reinterpret_cast<uint32_t*>(&h2);
+                  }
+                  *reinterpret_cast<uint4*>(rowp + ((q ^ ((c.tile_row >> 1) & 3)) << 4)) =
+                      make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                }
+              }
+            } else {
+              emit32(p, rbase, c.n0 + c.c0 + 32 * k, rq, y, amx);
+            }
           }
         }
-      }
+      };
+#ifdef SAMP_LN_ALWAYS_CLAMP
+      emit_rows(std::true_type{});
+#else
+      if (!I8_ONLY || !p.noclamp) emit_rows(std::true_type{});
+      else emit_rows(std::false_type{});
+#endif
     }
     if constexpr (!I8_ONLY) {
       if (p.tma_f) {   // three 32-column boxes of each staged output, one TMA store each

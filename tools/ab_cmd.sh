@@ -1,3 +1,4 @@
-timeout 300 python -m pytest tests/test_gpu_kernels.py -k gelu_fast_admission -x -q -s > gpurun_out/gadm_new.txt 2>&1
-SAMP_B200_LIB=abtest/flags/libsamp_b200.so timeout 300 python tools/gelu_flag_rate.py > gpurun_out/gflags.txt 2>&1
-bash tools/gelu_ab.sh marginv2 "c2 c4"
+# scratch A/B driver (edited per experiment): tests touching the change, then ab_lib.sh
+timeout 900 python -m pytest -q -x tests/test_gpu_tma_epilogues.py > gpurun_out/abt.log 2>&1; tail -1 gpurun_out/abt.log
+bash tools/ab_lib.sh "c2" base= lnclamp=abtest/lnclamp/libsamp_b200.so > gpurun_out/al_summary.txt 2>&1
+bash tools/ab_lat.sh "X=1" "SAMP_B200_LIB=abtest/lnclamp/libsamp_b200.so" 2 > gpurun_out/ab_lat.txt 2>&1

@@ -272,7 +272,9 @@ __device__ __forceinline__ float att_softmax(const AttnParams& p, const AttRow& 
   if (stamp) stamp[3] = globaltimer();
   const float2 negmx = f2(-mx, -mx), mm = f2(m, m);
 
-  // ---- pass 2: e = exp(x - max) -> TMEM (0 past S)
+  // ---- pass 2: e = exp(x - max) -> TMEM (0 past S).  The warp-uniform fast / exact choice
+  // is made once, outside the chunk loop, so the fast loop body stays compact
+#ifdef SAMP_ATT_PASS2_INLINE   // measurement: the round-2 form (choice inside the loop)
   for (int c0 = 32 * h; c0 < nrow; c0 += 32 * TPR) {
     uint32_t v[32];
     tmem_ld32(ta + kbeg + c0, v);
@@ -298,6 +300,39 @@ __device__ __forceinline__ float att_softmax(const AttnParams& p, const AttRow& 
     }
     tmem_st32(ta + kbeg + c0, v);
   }
+#else
+  if (fast) {
+    for (int c0 = 32 * h; c0 < nrow; c0 += 32 * TPR) {
+      uint32_t v[32];
+      tmem_ld32(ta + kbeg + c0, v);
+      tmem_wait_ld();
+      const bool clean = c0 + 32 <= att;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float2 x = mul2(acc_pair<F16>(v[j], v[j + 1], kx), mm, kx);
+        const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
+        v[j] = __float_as_uint(clean || c0 + j < att ? e.x : 0.0f);
+        v[j + 1] = __float_as_uint(clean || c0 + j + 1 < att ? e.y : 0.0f);
+      }
+      tmem_st32(ta + kbeg + c0, v);
+    }
+  } else {
+    for (int c0 = 32 * h; c0 < nrow; c0 += 32 * TPR) {
+      uint32_t v[32];
+      tmem_ld32(ta + kbeg + c0, v);
+      tmem_wait_ld();
+      // fully unrolled: a runtime index would put v[] in local memory
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int key = c0 + j;
+        float x = xval(as_acc(v[j]));
+        if (key >= att) x = __fadd_rn(x, ATT_MASK);
+        v[j] = __float_as_uint(key < S ? np_expf_nonpos(__fsub_rn(x, mx)) : 0.0f);
+      }
+      tmem_st32(ta + kbeg + c0, v);
+    }
+  }
+#endif
   tmem_wait_st();
   tc_fence_before();
   att_bar<TPR>();                               // every e of the row is in TMEM

@@ -306,13 +306,25 @@ __device__ __forceinline__ float att_softmax(const AttnParams& p, const AttRow& 
       uint32_t v[32];
       tmem_ld32(ta + kbeg + c0, v);
       tmem_wait_ld();
-      const bool clean = c0 + 32 <= att;
+#ifndef SAMP_ATT_CLEAN_SELECT
+      if (c0 + 32 <= att) {   // every key of the chunk unmasked: no per-key select
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float2 x = mul2(acc_pair<F16>(v[j], v[j + 1], kx), mm, kx);
-        const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
-        v[j] = __float_as_uint(clean || c0 + j < att ? e.x : 0.0f);
-        v[j + 1] = __float_as_uint(clean || c0 + j + 1 < att ? e.y : 0.0f);
+        for (int j = 0; j < 32; j += 2) {
+          const float2 x = mul2(acc_pair<F16>(v[j], v[j + 1], kx), mm, kx);
+          const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
+          v[j] = __float_as_uint(e.x);
+          v[j + 1] = __float_as_uint(e.y);
+        }
+      } else
+#endif
+      {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float2 x = mul2(acc_pair<F16>(v[j], v[j + 1], kx), mm, kx);
+          const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
+          v[j] = __float_as_uint(c0 + j < att ? e.x : 0.0f);
+          v[j + 1] = __float_as_uint(c0 + j + 1 < att ? e.y : 0.0f);
+        }
       }
       tmem_st32(ta + kbeg + c0, v);
     }

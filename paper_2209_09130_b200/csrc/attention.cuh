@@ -527,14 +527,25 @@ __device__ __forceinline__ void att_codes32(const uint32_t (&vc)[32], uint8_t* p
 // pass 2 of att_softmax_rr on one 32-key chunk held in registers (sequence-local keys
 // k0 .. k0+31), fast rows: e = numpy exp(x - max) by np_exp2_fast, 0 past att
 __device__ __forceinline__ void att_expo32_fast(uint32_t (&vc)[32], int k0, int att, float m, float mx, const X2& kx) {
-  const bool clean = k0 + 32 <= att;
   const float2 negmx = f2(-mx, -mx), mm = f2(m, m);
+#ifndef SAMP_ATT_CLEAN_SELECT
+  if (k0 + 32 <= att) {   // every key unmasked: no per-key select (as attention pass 2)
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const float2 x = mul2(acc_pair<false>(vc[j], vc[j + 1], kx), mm, kx);
+      const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
+      vc[j] = __float_as_uint(e.x);
+      vc[j + 1] = __float_as_uint(e.y);
+    }
+    return;
+  }
+#endif
 #pragma unroll
   for (int j = 0; j < 32; j += 2) {
     const float2 x = mul2(acc_pair<false>(vc[j], vc[j + 1], kx), mm, kx);
     const float2 e = np_exp2_fast(add2(x, negmx, kx), kx);
-    vc[j] = __float_as_uint(clean || k0 + j < att ? e.x : 0.0f);
-    vc[j + 1] = __float_as_uint(clean || k0 + j + 1 < att ? e.y : 0.0f);
+    vc[j] = __float_as_uint(k0 + j < att ? e.x : 0.0f);
+    vc[j + 1] = __float_as_uint(k0 + j + 1 < att ? e.y : 0.0f);
   }
 }
 

@@ -403,14 +403,26 @@ __device__ __forceinline__ float att_softmax(const AttnParams& p, const AttRow& 
         tmem_ld32(ta + c0, v);
         tmem_wait_ld();
         if constexpr (F16) {
+#ifndef SAMP_ATT_F16_P3_SELECT
+          if (key0 + 32 <= S && !p.amax) {   // all keys in the sequence, no calibration tap
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float2 pv = div_pair(f2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), rden_r, rden_ns);
-            const float a = key0 + j < S ? pv.x : 0.0f;
-            const float b = key0 + j + 1 < S ? pv.y : 0.0f;
-            if (w.live) amx_sm = fmaxf(amx_sm, fmaxf(a, b));
-            __half2 hv = __floats2half2_rn(a, b);
-            wv[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
+            for (int j = 0; j < 32; j += 2) {
+              const float2 pv = div_pair(f2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), rden_r, rden_ns);
+              __half2 hv = __floats2half2_rn(pv.x, pv.y);
+              wv[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+          } else
+#endif
+          {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float2 pv = div_pair(f2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), rden_r, rden_ns);
+              const float a = key0 + j < S ? pv.x : 0.0f;
+              const float b = key0 + j + 1 < S ? pv.y : 0.0f;
+              if (w.live) amx_sm = fmaxf(amx_sm, fmaxf(a, b));
+              __half2 hv = __floats2half2_rn(a, b);
+              wv[j / 2] = *reinterpret_cast<uint32_t*>(&hv);
+            }
           }
         } else {
           // probabilities are >= +0, so quantize's copysign(0.5, y) is +0.5.  Keys past S

@@ -691,32 +691,45 @@ struct EpiF16Out {
     const TanhTable* tt = reinterpret_cast<const TanhTable*>(c.table ? c.table : smem);
     const float* sbias = reinterpret_cast<const float*>(c.table ? smem : smem + sizeof(TanhTable));
     float amx = 0.0f;
+    // GELU and the calibration amax are per-launch switches: compiled into separate loop
+    // bodies (a runtime test inside the loop would only be predicated)
+    auto body = [&](auto gelu_tag, auto amax_tag) {
+      constexpr bool GELU = decltype(gelu_tag)::value, AMAX = decltype(amax_tag)::value;
 #pragma unroll 1
-    for (int col = 0; col < c.ncols; col += 32) {
-      const int gcol = c.n0 + c.c0 + col;
-      uint32_t r[32];
-      tmem_ld32(c.taddr + col, r);
-      float b[32];
-      load_smem32(sbias + c.c0 + col, b);
-      tmem_wait_ld();
-      uint32_t packed[16];
+      for (int col = 0; col < c.ncols; col += 32) {
+        const int gcol = c.n0 + c.c0 + col;
+        uint32_t r[32];
+        tmem_ld32(c.taddr + col, r);
+        float b[32];
+        load_smem32(sbias + c.c0 + col, b);
+        tmem_wait_ld();
+        uint32_t packed[16];
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float x0 = __fadd_rn(__uint_as_float(r[j]), b[j]);
-        float x1 = __fadd_rn(__uint_as_float(r[j + 1]), b[j + 1]);
-        if (p.gelu) {
-          x0 = gelu_ref(x0, tt);
-          x1 = gelu_ref(x1, tt);
+        for (int j = 0; j < 32; j += 2) {
+          float x0 = __fadd_rn(__uint_as_float(r[j]), b[j]);
+          float x1 = __fadd_rn(__uint_as_float(r[j + 1]), b[j + 1]);
+          if constexpr (GELU) {
+            x0 = gelu_ref(x0, tt);
+            x1 = gelu_ref(x1, tt);
+          }
+          if constexpr (AMAX)
+            if (c.row < c.M) amx = fmaxf(amx, fmaxf(fabsf(x0), fabsf(x1)));
+          __half2 h = __floats2half2_rn(x0, x1);
+          packed[j / 2] = *reinterpret_cast<uint32_t*>(&h);
         }
-        if (c.row < c.M) amx = fmaxf(amx, fmaxf(fabsf(x0), fabsf(x1)));
-        __half2 h = __floats2half2_rn(x0, x1);
-        packed[j / 2] = *reinterpret_cast<uint32_t*>(&h);
-      }
-      if (c.row < c.M) {
-        uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
+        if (c.row < c.M) {
+          uint4* dst = reinterpret_cast<uint4*>(p.out + size_t(c.row) * p.ldo + gcol);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+          for (int j = 0; j < 4; ++j) dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+        }
       }
+    };
+    if (p.gelu) {
+      if (p.amax) body(std::true_type{}, std::true_type{});
+      else body(std::true_type{}, std::false_type{});
+    } else {
+      if (p.amax) body(std::false_type{}, std::true_type{});
+      else body(std::false_type{}, std::false_type{});
     }
     if (p.amax) amax_commit(p.amax + p.site0 + (p.block_cols ? c.n0 / p.block_cols : 0), amx);
   }
